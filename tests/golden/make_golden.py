@@ -1,0 +1,90 @@
+"""Generate the committed golden vectors by running the REAL reference package.
+
+Run in the build container only (it imports ``/root/reference/pkg/src``, which
+does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every case stores the float32 sinogram handed to both implementations, the
+plan/filter parameters, and the reference's float64 outputs of
+``tomoblocks.fourier_bp.fbp`` (``fourier_bp.py:508-530``; kernel "bst" and,
+for some cases, "ss"), ``ramp_filter`` (``:490-505``) and ``bst_backproject``
+(``:435-461``).  numpy / scipy versions are recorded in ``versions.json``.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "..", ".."))
+
+from oracle.bst_oracle import SHEPP_LOGAN, ellipse_sinogram  # noqa: E402  (input synthesis only)
+
+from tomoblocks import fourier_bp as ref_fbp  # noqa: E402
+from tomoblocks.grids import AngleAxis, DetectorAxis, Sinogram  # noqa: E402
+
+
+def _case(name, sino, plan_kw, filt_kw=None, full_turn=False, ss=False):
+    sino = np.asarray(sino, dtype=np.float32)
+    n_ang, n_t = sino.shape
+    filt_kw = filt_kw or {}
+    n_theta = n_ang // 2 if full_turn else n_ang
+    y = Sinogram(DetectorAxis(n_t), AngleAxis(n_ang, full_turn=full_turn), sino.astype(np.float64))
+    plan = ref_fbp.BstPlan(n_t=n_t, n_theta=n_theta, **plan_kw)
+    fplan = ref_fbp.FilterPlan(**filt_kw)
+    out = {
+        "sino": sino,
+        "fbp_bst": ref_fbp.fbp(y, plan, fplan, kernel="bst").data,
+        "ramp": ref_fbp.ramp_filter(y, fplan).data,
+        "bst": ref_fbp.bst_backproject(y, plan).data,
+        "params": np.array(json.dumps({"plan": plan_kw, "filter": filt_kw,
+                                       "full_turn": full_turn, "n_theta": n_theta})),
+    }
+    if ss:
+        out["fbp_ss"] = ref_fbp.fbp(y, plan, fplan, kernel="ss").data
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: sino {sino.shape} -> {out['fbp_bst'].shape}")
+
+
+def main():
+    rng0 = np.random.default_rng(0)
+    rng1 = np.random.default_rng(1)
+    # cfg1: Shepp-Logan 256^2, 256 angles (BASELINE.json configs[0])
+    sl = ellipse_sinogram(SHEPP_LOGAN, 256, 256)
+    _case("shepp256", sl, {}, ss=True)
+    # off-centre ellipse + N(0, 0.05^2) noise (SURVEY.md 8d parity stress)
+    el = ellipse_sinogram([(1.0, 0.5, 0.4, 0.1, -0.05, 0.0)], 256, 256)
+    _case("ellipse_noise256", el + rng0.normal(0.0, 0.05, el.shape), {})
+    # white noise, non power-of-two detector, V != n_t
+    _case("white300x180", rng1.normal(0.0, 1.0, (180, 300)), {}, ss=True)
+    # output_n != n_t puts the Nyquist lines inside the disc
+    _case("outn128", sl, {"output_n": 128})
+    # odd output grid (no half-node modulation when n is odd)
+    sm = ellipse_sinogram(SHEPP_LOGAN, 65, 33)
+    _case("odd65x33_n63", sm, {"output_n": 63}, ss=True)
+    # nearest-neighbour gridding
+    _case("nearest256", sl, {"interp": "nearest"})
+    # apodized ramp, non-default KB window and sigma_min
+    _case("apod128", ellipse_sinogram(SHEPP_LOGAN, 128, 96),
+          {"kb_beta": 8.0, "kb_support": 0.15, "sigma_min_bins": 2},
+          {"kind": "ramp_apodized", "rolloff": 0.7})
+    # pad_factor 4: radial transform twice the ramp transform
+    _case("pad4_128", ellipse_sinogram(SHEPP_LOGAN, 128, 128), {"pad_factor": 4})
+    # full-turn input (2V angles on [0, 2pi)); plan must be explicit
+    ft = ellipse_sinogram(SHEPP_LOGAN, 128, 256, full_turn=True)
+    _case("fullturn128", ft + rng0.normal(0.0, 0.02, ft.shape), {}, full_turn=True, ss=True)
+    # tiny detector
+    _case("tiny16x12", rng1.normal(0.0, 1.0, (12, 16)), {}, ss=True)
+    import scipy
+    with open(os.path.join(HERE, "versions.json"), "w") as f:
+        json.dump({"numpy": np.__version__, "scipy": scipy.__version__,
+                   "reference": "tomoblocks (/root/reference/pkg)"}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
