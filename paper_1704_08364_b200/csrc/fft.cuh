@@ -1,0 +1,234 @@
+// fft.cuh -- register/shared-memory Stockham FFT building blocks for sm_100a.
+//
+// One length-N complex transform is owned by TPF = N/RPT threads, each holding
+// RPT = min(16, N) points in registers.  Layout contract (in and out):
+//
+//     thread t holds x[t + i*TPF] in v[i],  i < RPT
+//
+// Passes are radix-16 (two radix-4 stages with constant inner twiddles) with one
+// radix-2/4/8 remainder pass last.  The first pass reads its butterfly inputs
+// straight from registers and the last pass leaves its outputs in registers in
+// the same layout, so an N=4096 transform makes exactly two shared-memory round
+// trips.  Between passes data goes through a padded smem buffer
+// (index i -> i + i/16: conflict-free for the strided Stockham stores).
+//
+// Forward = exp(-2 pi i jk/N) (numpy.fft.fft), inverse = exp(+2 pi i jk/N)
+// without the 1/N (callers fold normalisation into their epilogues).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tb {
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+// multiply by W^{N/4}: -i (forward) / +i (inverse)
+template <bool INV>
+__device__ __forceinline__ float2 mul_q1(float2 a) {
+  return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
+
+// cos/sin(2 pi k / 16)
+struct Trig16 {
+  static constexpr float c[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                                  0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                                  -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                                  0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+  static constexpr float s[16] = {0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f,
+                                  1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                                  0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                                  -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f};
+};
+
+// v * W_R^E with compile-time R | 16 and E (forward sign unless INV)
+template <int R, int E, bool INV>
+__device__ __forceinline__ float2 twc(float2 v) {
+  constexpr int e = ((E % R) + R) % R;
+  if constexpr (e == 0) {
+    return v;
+  } else if constexpr (2 * e == R) {
+    return make_float2(-v.x, -v.y);
+  } else if constexpr (4 * e == R) {
+    return mul_q1<INV>(v);
+  } else if constexpr (4 * e == 3 * R) {
+    return mul_q1<!INV>(v);
+  } else if constexpr (8 * e == R || 8 * e == 3 * R || 8 * e == 5 * R || 8 * e == 7 * R) {
+    // odd multiples of pi/4: (+-1 +- i)/sqrt2 -> 2 adds + 2 muls
+    constexpr int k = e * (16 / R);
+    constexpr float c = Trig16::c[k];
+    constexpr float s = INV ? Trig16::s[k] : -Trig16::s[k];
+    // (x + iy)(c + is) with |c| = |s| = 1/sqrt2
+    constexpr float h = 0.70710678118654752f;
+    constexpr float sc = c > 0 ? 1.0f : -1.0f;
+    constexpr float ss = s > 0 ? 1.0f : -1.0f;
+    return make_float2((sc * v.x - ss * v.y) * h, (ss * v.x + sc * v.y) * h);
+  } else {
+    constexpr int k = e * (16 / R);
+    constexpr float c = Trig16::c[k];
+    constexpr float s = INV ? Trig16::s[k] : -Trig16::s[k];
+    return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
+  }
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft2(float2& a, float2& b) {
+  float2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(float2& x0, float2& x1, float2& x2, float2& x3) {
+  float2 a = cadd(x0, x2), b = csub(x0, x2), c = cadd(x1, x3), d = mul_q1<INV>(csub(x1, x3));
+  x0 = cadd(a, c);
+  x2 = csub(a, c);
+  x1 = cadd(b, d);
+  x3 = csub(b, d);
+}
+
+// In-register DFT of size R in natural order: v[k] <- sum_j v[j] W_R^{jk}.
+template <int R, bool INV>
+struct Dft;
+
+template <bool INV>
+struct Dft<1, INV> {
+  __device__ __forceinline__ static void run(float2*) {}
+};
+template <bool INV>
+struct Dft<2, INV> {
+  __device__ __forceinline__ static void run(float2* v) { dft2<INV>(v[0], v[1]); }
+};
+template <bool INV>
+struct Dft<4, INV> {
+  __device__ __forceinline__ static void run(float2* v) { dft4<INV>(v[0], v[1], v[2], v[3]); }
+};
+// R = 4*B: n = B*n1 + n2 ; k = k1 + 4*k2
+template <int R, bool INV>
+struct Dft {
+  static constexpr int B = R / 4;
+  __device__ __forceinline__ static void run(float2* v) {
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) dft4<INV>(v[n2], v[B + n2], v[2 * B + n2], v[3 * B + n2]);
+    // now v[B*k1 + n2] = Y[n2][k1]; twiddle by W_R^{n2*k1}
+    twiddle_all(v);
+    float2 o[R];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      float2 w[B];
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) w[n2] = v[B * k1 + n2];
+      Dft<B, INV>::run(w);
+#pragma unroll
+      for (int k2 = 0; k2 < B; ++k2) o[k1 + 4 * k2] = w[k2];
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) v[k] = o[k];
+  }
+  template <int I = 0>
+  __device__ __forceinline__ static void twiddle_all(float2* v) {
+    if constexpr (I < R) {
+      constexpr int k1 = I / B, n2 = I % B;
+      v[I] = twc<R, n2 * k1, INV>(v[I]);
+      twiddle_all<I + 1>(v);
+    }
+  }
+};
+
+__device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
+
+template <int N>
+struct FftShape {
+  static_assert((N & (N - 1)) == 0 && N >= 2, "power of two");
+  static constexpr int RPT = N < 16 ? N : 16;  // points per thread
+  static constexpr int TPF = N / RPT;          // threads per transform
+  static constexpr int P = ilog2(N);
+  static constexpr int N16 = N >= 16 ? P / 4 : 0;                   // radix-16 passes
+  static constexpr int REM = N >= 16 ? (1 << (P % 4)) : N;          // remainder radix (last)
+  static constexpr int NPASS = N >= 16 ? N16 + (REM > 1 ? 1 : 0) : 1;
+  static constexpr int SMEM = NPASS > 1 ? N + N / 16 : 0;          // float2 elements
+  __host__ __device__ static constexpr int radix(int p) { return N < 16 ? N : (p < N16 ? 16 : REM); }
+  __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
+};
+
+// One Stockham pass.  tw[j] = exp(-2 pi i j / N) for j < N (fp32).
+template <int N, int PASS, bool INV>
+__device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* buf, int t,
+                                         const float2* __restrict__ tw) {
+  using S = FftShape<N>;
+  constexpr int R = S::radix(PASS);
+  constexpr int NS = S::ns(PASS);
+  constexpr int NB = N / R;
+  constexpr int PER = S::RPT / R;
+  constexpr bool FIRST = PASS == 0;
+  constexpr bool LAST = PASS == S::NPASS - 1;
+  float2 x[PER][R];
+#pragma unroll
+  for (int b = 0; b < PER; ++b)
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      if constexpr (FIRST) x[b][m] = v[b + m * PER];
+      else x[b][m] = buf[spad(t + b * S::TPF + m * NB)];
+    }
+  if constexpr (!FIRST) __syncthreads();
+#pragma unroll
+  for (int b = 0; b < PER; ++b) {
+    const int j = t + b * S::TPF;
+    const int k = j & (NS - 1);
+    if constexpr (NS > 1) {
+      float2 w = __ldg(&tw[k * (N / (NS * R))]);
+      if (INV) w.y = -w.y;
+      float2 wp[R];
+      wp[1] = w;
+#pragma unroll
+      for (int m = 2; m < R; ++m) wp[m] = (m & 1) ? cmul(wp[m - 1], wp[1]) : cmul(wp[m / 2], wp[m / 2]);
+#pragma unroll
+      for (int m = 1; m < R; ++m) x[b][m] = cmul(x[b][m], wp[m]);
+    }
+    Dft<R, INV>::run(x[b]);
+    if constexpr (LAST) {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[b + m * PER] = x[b][m];
+    } else {
+      const int base = (j / NS) * NS * R + k;
+#pragma unroll
+      for (int m = 0; m < R; ++m) buf[spad(base + m * NS)] = x[b][m];
+    }
+  }
+  if constexpr (!LAST) __syncthreads();
+}
+
+template <int N, bool INV, int PASS = 0>
+__device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
+                                           const float2* __restrict__ tw) {
+  if constexpr (PASS < FftShape<N>::NPASS) {
+    constexpr bool LAST = PASS == FftShape<N>::NPASS - 1;
+    constexpr bool FIRST = PASS == 0;
+    if (active) {
+      fft_pass<N, PASS, INV>(v, buf, t, tw);
+    } else {
+      // keep the CTA-wide barriers balanced for idle threads
+      if constexpr (!FIRST) __syncthreads();
+      if constexpr (!LAST) __syncthreads();
+    }
+    fft_passes<N, INV, PASS + 1>(v, buf, t, active, tw);
+  }
+}
+
+// Full transform.  Must be called by every thread of the CTA (barriers);
+// threads with !active only take part in the barriers.  On return the
+// buffer may be reused only after a __syncthreads().
+template <int N, bool INV>
+__device__ __forceinline__ void fft(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
+                                    const float2* __restrict__ tw) {
+  fft_passes<N, INV, 0>(v, buf, t, active, tw);
+}
+
+}  // namespace tb

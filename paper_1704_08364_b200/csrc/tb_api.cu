@@ -1,0 +1,672 @@
+// tb_api.cu -- host side of the C ABI declared in include/tb_bst.h.
+//
+// Plan creation restates the reference's BstPlan / FilterPlan derived tables
+// (fourier_bp.py:97-267) in float64 on the host and uploads them once; the
+// execute functions only enqueue kernels on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tb_bst.h"
+#include "tb_kernels.cuh"
+
+using tb::DevPlan;
+using tb::Work;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define TB_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(TB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr int kMaxL = 8192;
+
+int next_pow2(long n) {
+  long m = 1;
+  while (m < n) m *= 2;
+  return (int)m;
+}
+
+// Modified Bessel I0 by its power series (scipy.special.i0 in the reference,
+// fourier_bp.py:187); converges to fp64 accuracy for the betas of interest.
+double bessel_i0(double x) {
+  const double y = 0.25 * x * x;
+  double term = 1.0, sum = 1.0;
+  for (int k = 1; k < 500; ++k) {
+    term *= y / ((double)k * (double)k);
+    sum += term;
+    if (term < sum * 1e-17) break;
+  }
+  return sum;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+struct tb_plan {
+  tb_plan_desc desc;
+  int device;
+  int n_t, V, rows, L, H, n, npad, lo, hi, S;
+  double amp;
+  int groups, pairs_per_cta;
+  DevPlan dp;
+  void* blob = nullptr;  // all device tables in one allocation
+};
+
+namespace {
+
+struct Layout {
+  size_t polar, rowcoef, part, common, coefmean, columns, filtered, status, total;
+};
+
+Layout layout_for(const tb_plan* p, int B) {
+  Layout l;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  l.status = take(2 * sizeof(int));  // first: its offset does not depend on the batch
+  l.polar = take((size_t)B * p->rows * p->H * sizeof(float2));
+  l.rowcoef = take((size_t)B * p->rows * sizeof(float));
+  l.part = take((size_t)B * p->groups * std::max(p->S, 1) * sizeof(float));
+  l.common = take((size_t)B * p->H * sizeof(float2));
+  l.coefmean = take((size_t)B * sizeof(float));
+  l.columns = take((size_t)B * (p->H + 1) * p->n * sizeof(float2));
+  l.filtered = take((size_t)B * p->rows * p->n_t * sizeof(float));
+  l.total = off;
+  return l;
+}
+
+Work work_for(const tb_plan* p, int B, void* ws) {
+  Layout l = layout_for(p, B);
+  char* base = static_cast<char*>(ws);
+  Work w;
+  w.polar = reinterpret_cast<float2*>(base + l.polar);
+  w.rowcoef = reinterpret_cast<float*>(base + l.rowcoef);
+  w.part = reinterpret_cast<float*>(base + l.part);
+  w.common = reinterpret_cast<float2*>(base + l.common);
+  w.coefmean = reinterpret_cast<float*>(base + l.coefmean);
+  w.columns = reinterpret_cast<float2*>(base + l.columns);
+  w.filtered = reinterpret_cast<float*>(base + l.filtered);
+  w.status = reinterpret_cast<int*>(base + l.status);
+  w.groups = p->groups;
+  w.pairs_per_cta = p->pairs_per_cta;
+  return w;
+}
+
+// ---------------------------------------------------------------------------
+// per-L launchers
+// ---------------------------------------------------------------------------
+template <int L>
+struct Launch {
+  using K = tb::KShape<L>;
+  static size_t smem_k1(const tb_plan* p) { return K::BUF * sizeof(float2) + (size_t)std::max(p->S, 1) * 4; }
+  static size_t smem_k1b(const tb_plan* p) {
+    return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::THREADS * 4;
+  }
+  static size_t smem_fft() { return K::BUF * sizeof(float2); }
+
+  static int configure(const tb_plan* p) {
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    return TB_OK;
+  }
+
+  // one launch group of B slices through K1 -> K1b -> K2 -> K3
+  static int bst_group(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp,
+                       float out_scale, cudaStream_t st) {
+    const DevPlan& dp = p->dp;
+    const float* k1_in = sino;
+    bool fused = false;
+    if (ramp) {
+      if (p->npad == L) {
+        fused = true;
+      } else {
+        int rc = ramp_rows(p, sino, w.filtered, B * p->rows, w, st);
+        if (rc) return rc;
+        k1_in = w.filtered;
+      }
+    }
+    dim3 g1(p->groups, B);
+    if (fused)
+      tb::k1_radial<L, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    else
+      tb::k1_radial<L, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    tb::k1b_common<L><<<B, K::THREADS, smem_k1b(p), st>>>(dp, w);
+    tb::k2_columns<L><<<dim3(p->H + 1, B), K::THREADS, smem_fft(), st>>>(dp, w);
+    tb::k3_rows<L><<<dim3((p->n + 1) / 2, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
+    TB_CUDA(cudaGetLastError());
+    return TB_OK;
+  }
+
+  static int ramp_rows(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,
+                       cudaStream_t st);
+};
+
+template <int NP>
+int launch_ramp(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
+  using K = tb::KShape<NP>;
+  tb::kr_ramp<NP><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int ramp_dispatch(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
+  switch (p->npad) {
+#define TB_CASE(N) \
+  case N:          \
+    return launch_ramp<N>(p, in, out, total_rows, w, st);
+    TB_CASE(4) TB_CASE(8) TB_CASE(16) TB_CASE(32) TB_CASE(64) TB_CASE(128) TB_CASE(256) TB_CASE(512)
+    TB_CASE(1024) TB_CASE(2048) TB_CASE(4096) TB_CASE(8192)
+#undef TB_CASE
+  }
+  return fail(TB_ERR_UNSUPPORTED, "ramp length not supported on the GPU path");
+}
+
+template <int L>
+int Launch<L>::ramp_rows(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,
+                         cudaStream_t st) {
+  return ramp_dispatch(p, in, out, total_rows, w, st);
+}
+
+#define TB_DISPATCH_L(Lval, EXPR_TEMPLATE)                                                   \
+  switch (Lval) {                                                                           \
+    case 4: { constexpr int L_ = 4; return EXPR_TEMPLATE; }                                 \
+    case 8: { constexpr int L_ = 8; return EXPR_TEMPLATE; }                                 \
+    case 16: { constexpr int L_ = 16; return EXPR_TEMPLATE; }                               \
+    case 32: { constexpr int L_ = 32; return EXPR_TEMPLATE; }                               \
+    case 64: { constexpr int L_ = 64; return EXPR_TEMPLATE; }                               \
+    case 128: { constexpr int L_ = 128; return EXPR_TEMPLATE; }                             \
+    case 256: { constexpr int L_ = 256; return EXPR_TEMPLATE; }                             \
+    case 512: { constexpr int L_ = 512; return EXPR_TEMPLATE; }                             \
+    case 1024: { constexpr int L_ = 1024; return EXPR_TEMPLATE; }                           \
+    case 2048: { constexpr int L_ = 2048; return EXPR_TEMPLATE; }                           \
+    case 4096: { constexpr int L_ = 4096; return EXPR_TEMPLATE; }                           \
+    case 8192: { constexpr int L_ = 8192; return EXPR_TEMPLATE; }                           \
+  }                                                                                         \
+  return fail(TB_ERR_UNSUPPORTED, "radial_samples not supported on the GPU path");
+
+int configure_dispatch(const tb_plan* p) { TB_DISPATCH_L(p->L, Launch<L_>::configure(p)) }
+
+int bst_dispatch(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp, float scale,
+                 cudaStream_t st) {
+  TB_DISPATCH_L(p->L, Launch<L_>::bst_group(p, sino, img, B, w, ramp, scale, st))
+}
+
+int check_exec_args(const tb_plan* p, const void* a, const void* b, int n_slices, int batch, const void* ws,
+                    size_t ws_bytes) {
+  if (!p) return fail(TB_ERR_INVALID, "null plan");
+  if (n_slices < 0) return fail(TB_ERR_INVALID, "n_slices must be >= 0");
+  if (n_slices > 0 && (!a || !b)) return fail(TB_ERR_INVALID, "null data pointer");
+  if (batch < 1) return fail(TB_ERR_INVALID, "batch must be >= 1");
+  if (ws) {
+    size_t need = layout_for(p, batch).total;
+    if (ws_bytes < need)
+      return fail(TB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes, got " +
+                                        std::to_string(ws_bytes));
+  } else {
+    return fail(TB_ERR_WORKSPACE, "null workspace");
+  }
+  return TB_OK;
+}
+
+int set_device(const tb_plan* p) {
+  int cur = -1;
+  TB_CUDA(cudaGetDevice(&cur));
+  if (cur != p->device) TB_CUDA(cudaSetDevice(p->device));
+  return TB_OK;
+}
+
+int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, int batch, void* ws,
+                 size_t ws_bytes, void* stream, bool ramp, float scale) {
+  int rc = check_exec_args(p, sino, img, n_slices, batch, ws, ws_bytes);
+  if (rc) return rc;
+  if ((rc = set_device(p))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t in_stride = (size_t)p->rows * p->n_t;
+  const size_t out_stride = (size_t)p->n * p->n;
+  for (int s0 = 0; s0 < n_slices; s0 += batch) {
+    const int B = std::min(batch, n_slices - s0);
+    Work w = work_for(p, batch, ws);
+    rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, st);
+    if (rc) return rc;
+  }
+  return TB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int tb_abi_version(void) { return TB_ABI_VERSION; }
+
+const char* tb_last_error(void) { return g_err.c_str(); }
+
+int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
+  if (!d || !out) return fail(TB_ERR_INVALID, "null argument");
+  *out = nullptr;
+  // --- validation: same rules and messages as BstPlan.__post_init__
+  //     (fourier_bp.py:88-109) and FilterPlan.__post_init__ (:259-263)
+  if (d->n_t < 2 || d->n_theta < 1) return fail(TB_ERR_INVALID, "need n_t >= 2 and n_theta >= 1");
+  if (d->pad_factor < 2)
+    return fail(TB_ERR_INVALID, "pad_factor must be >= 2, got " + std::to_string(d->pad_factor));
+  if (d->sigma_min_bins < 1)
+    return fail(TB_ERR_INVALID, "sigma_min_bins must be >= 1, got " + std::to_string(d->sigma_min_bins));
+  if (d->interp != TB_INTERP_BILINEAR && d->interp != TB_INTERP_NEAREST)
+    return fail(TB_ERR_INVALID, "unknown interp mode");
+  long L = d->radial_samples > 0 ? d->radial_samples : next_pow2((long)d->pad_factor * d->n_t);
+  if ((L & (L - 1)) || L < (long)d->pad_factor * d->n_t)
+    return fail(TB_ERR_INVALID, "radial_samples must be a power of two >= pad_factor * n_t, got " +
+                                    std::to_string(L));
+  const int n = d->output_n > 0 ? d->output_n : d->n_t;
+  if (n < 1 || n > L) return fail(TB_ERR_INVALID, "output_n must be in [1, radial_samples]");
+  if (d->filter_kind != TB_FILTER_RAMP && d->filter_kind != TB_FILTER_RAMP_APODIZED)
+    return fail(TB_ERR_INVALID, "unknown filter kind");
+  if (!(d->rolloff > 0.0 && d->rolloff <= 1.0))
+    return fail(TB_ERR_INVALID, "rolloff must be in (0, 1]");
+  if (!(d->kb_support > 0.0)) return fail(TB_ERR_INVALID, "kb_support must be > 0");
+  if (L > kMaxL) return fail(TB_ERR_UNSUPPORTED, "radial_samples > 8192 is not supported on the GPU path");
+
+  tb_plan* p = new tb_plan();
+  p->desc = *d;
+  p->device = device;
+  p->n_t = d->n_t;
+  p->V = d->n_theta;
+  p->rows = d->full_turn ? 2 * d->n_theta : d->n_theta;
+  p->L = (int)L;
+  p->H = (int)L / 2;
+  p->n = n;
+  p->npad = 2 * next_pow2(d->n_t);
+  const int n_t = p->n_t, V = p->V, H = p->H;
+  const int npad = p->npad;
+
+  // --- scalar geometry (fourier_bp.py:119-152)
+  const double dt = 2.0 / (n_t - 1);
+  const double df = 1.0 / (L * dt);
+  const double sigma_min = d->sigma_min_bins * df;
+  const double du = 2.0 / n;
+  const double dnu = 1.0 / (L * du);
+  p->amp = (dnu * L) * (dnu * L) * dt;
+
+  // --- KB window (fourier_bp.py:180-190) and its support, closed under i -> n_t-1-i
+  std::vector<double> bump(n_t, 0.0);
+  const double i0b = bessel_i0(d->kb_beta);
+  int lo = n_t, hi = -1;
+  for (int i = 0; i < n_t; ++i) {
+    const double t = -1.0 + 2.0 * i / (n_t - 1);
+    if (std::fabs(t) <= d->kb_support) {
+      const double x = std::max(1.0 - (t / d->kb_support) * (t / d->kb_support), 0.0);
+      bump[i] = bessel_i0(d->kb_beta * std::sqrt(x)) / i0b;
+      lo = std::min(lo, i);
+      hi = std::max(hi, i);
+    }
+  }
+  if (hi >= lo) {
+    const int lo2 = std::min(lo, n_t - 1 - hi), hi2 = std::max(hi, n_t - 1 - lo);
+    lo = lo2;
+    hi = hi2;
+  } else {
+    lo = 0;
+    hi = -1;
+  }
+  p->lo = lo;
+  p->hi = hi;
+  p->S = hi - lo + 1;
+
+  // --- K1 work split: <= 128 CTAs (partial-sum groups) per slice
+  const int npairs = (p->rows + 1) / 2;
+  p->pairs_per_cta = std::max(1, (npairs + 127) / 128);
+  p->groups = (npairs + p->pairs_per_cta - 1) / p->pairs_per_cta;
+
+  // --- host tables
+  auto tw = [](int N) {
+    std::vector<float2> v(N);
+    for (int j = 0; j < N; ++j) {
+      const double a = 2.0 * kPi * (double)j / N;
+      v[j] = make_float2((float)std::cos(a), (float)-std::sin(a));
+    }
+    return v;
+  };
+  std::vector<float2> twL = tw((int)L), twN = tw(npad);
+
+  // ramp multiplier 2 pi |f| (x raised-cosine taper) / npad (fourier_bp.py:477-487)
+  std::vector<float> g(npad);
+  {
+    const double val = 1.0 / (npad * dt);
+    const double fnyq = (npad / 2) * val;
+    const bool apod = d->filter_kind == TB_FILTER_RAMP_APODIZED && d->rolloff < 1.0;
+    for (int k = 0; k < npad; ++k) {
+      const int kk = std::min(k, npad - k);
+      const double f = kk * val;
+      double m = 2.0 * kPi * std::fabs(f);
+      if (apod) {
+        const double start = d->rolloff * fnyq;
+        if (f > start) {
+          const double frac = (f - start) / ((1.0 - d->rolloff) * fnyq);
+          m *= 0.5 * (1.0 + std::cos(kPi * frac));
+        }
+      }
+      g[k] = (float)(m / npad);
+    }
+  }
+  std::vector<float> omb(n_t), bump_s(std::max(p->S, 1), 0.f);
+  for (int i = 0; i < n_t; ++i) omb[i] = (float)(1.0 - bump[i]);
+  for (int s = 0; s < p->S; ++s) bump_s[s] = (float)bump[lo + s];
+
+  // true-origin phase, reference spectrum and kernel denominator over k < H
+  // (fourier_bp.py:164-202, 372): S_k = exp(2 pi i f_k) sum_i w_i exp(-2 pi i k i / L)
+  std::vector<float2> psi(H), rho(H);
+  {
+    const double val = 1.0 / (L * dt);
+    for (int k = 0; k < H; ++k) {
+      const double f = k * val;
+      const double den = std::max(std::fabs(f), sigma_min);
+      const double ph = 2.0 * kPi * f;
+      const double pr = std::cos(ph), pim = std::sin(ph);
+      double sr, si;
+      if (k == 0) {
+        sr = n_t;
+        si = 0.0;
+      } else {
+        // sum_{i<n_t} z^i with z = exp(-2 pi i k / L)
+        const double a1 = -2.0 * kPi * (double)k / L;
+        const double an = -2.0 * kPi * (double)(((long long)k * n_t) % L) / L;
+        const double nr = 1.0 - std::cos(an), ni = -std::sin(an);
+        const double dr = 1.0 - std::cos(a1), di = -std::sin(a1);
+        const double dd = dr * dr + di * di;
+        sr = (nr * dr + ni * di) / dd;
+        si = (ni * dr - nr * di) / dd;
+      }
+      psi[k] = make_float2((float)(pr / den), (float)(pim / den));
+      rho[k] = make_float2((float)((pr * sr - pim * si) / den), (float)((pr * si + pim * sr) / den));
+    }
+  }
+  // half-node modulation (fourier_bp.py:424-430)
+  std::vector<float2> modt(L, make_float2(1.f, 0.f));
+  int has_mod = 0;
+  {
+    const long m0 = L / 2 - n / 2;
+    const double delta = (-1.0 + 1.0 / n) - (double)(m0 - L / 2) * du;
+    if (delta != 0.0) {
+      has_mod = 1;
+      for (long k = 0; k < L; ++k) {
+        const long ks = k < L / 2 ? k : k - L;
+        const double a = 2.0 * kPi * ((double)ks * dnu) * delta;
+        modt[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+    }
+  }
+  // tabulated angles u * pi / V for the octant-reduced residual (double-float)
+  const int nang = V / 4 + 3;
+  std::vector<float4> angtab(nang);
+  for (int u = 0; u < nang; ++u) {
+    const double th = (double)u * kPi / V;
+    const double c = std::cos(th), s = std::sin(th);
+    const float ch = (float)c, sh = (float)s;
+    angtab[u] = make_float4(ch, (float)(c - ch), sh, (float)(s - sh));
+  }
+  // slant-stack angles (grids.py:85-95; projector.py:137-141)
+  const int A = p->rows;
+  const double span = d->full_turn ? 2.0 * kPi : kPi;
+  std::vector<double2> sscs(A);
+  for (int j = 0; j < A; ++j) {
+    const double th = (double)j * (span / A);
+    sscs[j] = make_double2(std::cos(th), std::sin(th));
+  }
+
+  // --- upload everything in one allocation
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  const size_t o_twL = take(twL.size() * sizeof(float2));
+  const size_t o_twN = take(twN.size() * sizeof(float2));
+  const size_t o_g = take(g.size() * sizeof(float));
+  const size_t o_omb = take(omb.size() * sizeof(float));
+  const size_t o_bs = take(bump_s.size() * sizeof(float));
+  const size_t o_psi = take(psi.size() * sizeof(float2));
+  const size_t o_rho = take(rho.size() * sizeof(float2));
+  const size_t o_mod = take(modt.size() * sizeof(float2));
+  const size_t o_ang = take(angtab.size() * sizeof(float4));
+  const size_t o_ss = take(sscs.size() * sizeof(double2));
+  std::vector<char> host(off, 0);
+  auto put = [&](size_t o, const void* src, size_t bytes) { std::memcpy(host.data() + o, src, bytes); };
+  put(o_twL, twL.data(), twL.size() * sizeof(float2));
+  put(o_twN, twN.data(), twN.size() * sizeof(float2));
+  put(o_g, g.data(), g.size() * sizeof(float));
+  put(o_omb, omb.data(), omb.size() * sizeof(float));
+  put(o_bs, bump_s.data(), bump_s.size() * sizeof(float));
+  put(o_psi, psi.data(), psi.size() * sizeof(float2));
+  put(o_rho, rho.data(), rho.size() * sizeof(float2));
+  put(o_mod, modt.data(), modt.size() * sizeof(float2));
+  put(o_ang, angtab.data(), angtab.size() * sizeof(float4));
+  put(o_ss, sscs.data(), sscs.size() * sizeof(double2));
+
+  int prev = -1;
+  cudaGetDevice(&prev);
+  auto cleanup = [&](int code, const std::string& msg) {
+    if (p->blob) cudaFree(p->blob);
+    delete p;
+    if (prev >= 0) cudaSetDevice(prev);
+    return fail(code, msg);
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  e = cudaMalloc(&p->blob, off);
+  if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  e = cudaMemcpy(p->blob, host.data(), off, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+  char* b = static_cast<char*>(p->blob);
+
+  DevPlan& dp = p->dp;
+  dp.n_t = n_t;
+  dp.n_theta = V;
+  dp.rows = p->rows;
+  dp.L = (int)L;
+  dp.H = H;
+  dp.n = n;
+  dp.npad = npad;
+  dp.lo = lo;
+  dp.S = p->S;
+  dp.full_turn = d->full_turn ? 1 : 0;
+  dp.interp = d->interp;
+  const double cr = dnu / df;
+  // Nyquist lines can hold in-disc nodes only if H*cr <= H - 1 (+1/2 for rounding)
+  dp.nyq = (H * cr <= (H - 1) + 0.5 + 1e-9) ? 1 : 0;
+  dp.has_mod = has_mod;
+  dp.n_half = n / 2;
+  dp.inv_nt = (float)(1.0 / n_t);
+  dp.cr_hi = (float)cr;
+  dp.cr_lo = (float)(cr - (double)dp.cr_hi);
+  dp.vpi = (float)(V / kPi);
+  dp.inv_rows2 = (float)(1.0 / (2.0 * V));
+  dp.img_scale = (float)(p->amp / ((double)L * (double)L));
+  dp.ss_weight = (float)(span / A);
+  dp.ss_inv_dt = (float)(1.0 / dt);
+  dp.tw_L = reinterpret_cast<const float2*>(b + o_twL);
+  dp.tw_np = reinterpret_cast<const float2*>(b + o_twN);
+  dp.ramp_g = reinterpret_cast<const float*>(b + o_g);
+  dp.omb = reinterpret_cast<const float*>(b + o_omb);
+  dp.bump_s = reinterpret_cast<const float*>(b + o_bs);
+  dp.psi = reinterpret_cast<const float2*>(b + o_psi);
+  dp.rho = reinterpret_cast<const float2*>(b + o_rho);
+  dp.modt = reinterpret_cast<const float2*>(b + o_mod);
+  dp.angtab = reinterpret_cast<const float4*>(b + o_ang);
+  dp.ss_cs = reinterpret_cast<const double2*>(b + o_ss);
+
+  int rc = configure_dispatch(p);
+  if (rc) {
+    std::string m = g_err;
+    return cleanup(rc, m);
+  }
+  if (prev >= 0 && prev != device) cudaSetDevice(prev);
+  *out = p;
+  return TB_OK;
+}
+
+int tb_plan_destroy(tb_plan* p) {
+  if (!p) return TB_OK;
+  if (p->blob) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    cudaFree(p->blob);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete p;
+  return TB_OK;
+}
+
+int tb_plan_get_info(const tb_plan* p, tb_plan_info* info) {
+  if (!p || !info) return fail(TB_ERR_INVALID, "null argument");
+  info->n_t = p->n_t;
+  info->n_theta = p->V;
+  info->n_angles = p->rows;
+  info->radial_samples = p->L;
+  info->ramp_samples = p->npad;
+  info->output_n = p->n;
+  info->support_lo = p->lo;
+  info->support_hi = p->hi;
+  info->amplitude_scale = p->amp;
+  return TB_OK;
+}
+
+int tb_workspace_bytes(const tb_plan* p, int batch, size_t* bytes) {
+  if (!p || !bytes) return fail(TB_ERR_INVALID, "null argument");
+  if (batch < 1) return fail(TB_ERR_INVALID, "batch must be >= 1");
+  *bytes = layout_for(p, batch).total;
+  return TB_OK;
+}
+
+int tb_workspace_get_layout(const tb_plan* p, int batch, tb_workspace_layout* out) {
+  if (!p || !out) return fail(TB_ERR_INVALID, "null argument");
+  if (batch < 1) return fail(TB_ERR_INVALID, "batch must be >= 1");
+  Layout l = layout_for(p, batch);
+  out->total = l.total;
+  out->polar = l.polar;
+  out->rowcoef = l.rowcoef;
+  out->common = l.common;
+  out->coefmean = l.coefmean;
+  out->columns = l.columns;
+  out->filtered = l.filtered;
+  out->status = l.status;
+  return TB_OK;
+}
+
+int tb_fbp(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws, size_t ws_bytes,
+           void* stream) {
+  return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)));
+}
+
+int tb_bst(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws, size_t ws_bytes,
+           void* stream) {
+  return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, false, 1.0f);
+}
+
+int tb_ramp(const tb_plan* p, const float* sino, float* out, int n_slices, void* stream) {
+  if (!p) return fail(TB_ERR_INVALID, "null plan");
+  if (n_slices < 0) return fail(TB_ERR_INVALID, "n_slices must be >= 0");
+  if (n_slices == 0) return TB_OK;
+  if (!sino || !out) return fail(TB_ERR_INVALID, "null data pointer");
+  int rc = set_device(p);
+  if (rc) return rc;
+  Work w{};
+  w.status = nullptr;
+  return ramp_dispatch(p, sino, out, n_slices * p->rows, w, static_cast<cudaStream_t>(stream));
+}
+
+int tb_ss(const tb_plan* p, const float* sino, float* image, int n_slices, float scale, void* stream) {
+  if (!p) return fail(TB_ERR_INVALID, "null plan");
+  if (n_slices < 0) return fail(TB_ERR_INVALID, "n_slices must be >= 0");
+  if (n_slices == 0) return TB_OK;
+  if (!sino || !image) return fail(TB_ERR_INVALID, "null data pointer");
+  int rc = set_device(p);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Work w{};
+  w.status = nullptr;  // no workspace: the caller validates finiteness
+  const int n = p->n;
+  dim3 grid((n + 15) / 16, (n + 15) / 16, 1);
+  for (int s = 0; s < n_slices; s += 65535) {
+    const int B = std::min(65535, n_slices - s);
+    grid.z = B;
+    tb::k5_slant<<<grid, 256, 0, st>>>(p->dp, sino + (size_t)s * p->rows * p->n_t, p->rows,
+                                       image + (size_t)s * n * n, scale, w);
+  }
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_fbp_ss(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws,
+              size_t ws_bytes, void* stream) {
+  int rc = check_exec_args(p, sino, image, n_slices, batch, ws, ws_bytes);
+  if (rc) return rc;
+  if ((rc = set_device(p))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int n = p->n;
+  for (int s0 = 0; s0 < n_slices; s0 += batch) {
+    const int B = std::min(batch, n_slices - s0);
+    Work w = work_for(p, batch, ws);
+    rc = ramp_dispatch(p, sino + (size_t)s0 * p->rows * p->n_t, w.filtered, B * p->rows, w, st);
+    if (rc) return rc;
+    dim3 grid((n + 15) / 16, (n + 15) / 16, B);
+    tb::k5_slant<<<grid, 256, 0, st>>>(p->dp, w.filtered, p->rows, image + (size_t)s0 * n * n,
+                                       (float)(1.0 / (2.0 * kPi)), w);
+    TB_CUDA(cudaGetLastError());
+  }
+  return TB_OK;
+}
+
+int tb_reset_status(const tb_plan* p, void* ws, void* stream) {
+  if (!p || !ws) return fail(TB_ERR_INVALID, "null argument");
+  int rc = set_device(p);
+  if (rc) return rc;
+  Layout l = layout_for(p, 1);
+  TB_CUDA(cudaMemsetAsync(static_cast<char*>(ws) + l.status, 0, 2 * sizeof(int),
+                          static_cast<cudaStream_t>(stream)));
+  return TB_OK;
+}
+
+int tb_read_status(const tb_plan* p, const void* ws, void* stream) {
+  if (!p || !ws) return fail(TB_ERR_INVALID, "null argument");
+  int rc = set_device(p);
+  if (rc) return rc;
+  Layout l = layout_for(p, 1);
+  int h[2] = {0, 0};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  TB_CUDA(cudaMemcpyAsync(h, static_cast<const char*>(ws) + l.status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  TB_CUDA(cudaStreamSynchronize(st));
+  if (h[0]) return fail(TB_ERR_NONFINITE_INPUT, "sinogram contains non-finite values");
+  if (h[1]) return fail(TB_ERR_NONFINITE_OUTPUT, "non-finite values in backprojection output");
+  return TB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,580 @@
+// tb_kernels.cuh -- the BST filtered-backprojection kernels (sm_100a).
+//
+//   K1   k1_radial   per row pair: [ramp FFT -> x2 pi|f| -> IFFT] -> x(1-bump)
+//                    -> FFT_L -> split the two packed rows -> true-origin phase,
+//                    rect split and 1/max(|f|, sigma_min)      (fourier_bp.py:302-373, 469-505)
+//   K1b  k1b_common  per slice: angular mean row over the window support ->
+//                    common row Chat and coef.mean()          (fourier_bp.py:336-341, 452-458)
+//   K2   k2_columns  per Cartesian column k1: bilinear polar->Cartesian gather of
+//                    the Hermitian half plane (+ modulation) -> IFFT_L along k2,
+//                    pruned to the n output rows              (fourier_bp.py:376-431)
+//   K3   k3_rows     per output row pair: C2R along k1, crop, amplitude scale,
+//                    coverage add-back, 1/(2 pi), finite flag (fourier_bp.py:431-460, 530)
+//   KR   kr_ramp     standalone ramp filter                   (fourier_bp.py:490-505)
+//   K5   k5_slant    slant-stack comparator                   (projector.py:126-158)
+//
+// Layouts in HBM (fp32 / complex64):
+//   sino    [B][A][n_t]        A = input angles (n_theta, or 2 n_theta full turn)
+//   polar   [B][rows][H]       rows = processed angles = A, H = L/2 radial bins
+//   part    [B][groups][S]     per-CTA partial column sums over the KB support
+//   rowcoef [B][rows], common [B][H], coefmean [B]
+//   columns [B][H+1][n]        K2 output, k1-major
+//   image   [B][n][n]
+#pragma once
+#include "fft.cuh"
+
+namespace tb {
+
+struct DevPlan {
+  int n_t, n_theta, rows, L, H, n, npad;
+  int lo, S;          // KB window support [lo, lo+S)
+  int full_turn, interp, nyq;
+  int has_mod;
+  int n_half;         // n/2 (crop offset)
+  float inv_nt;
+  float cr_hi, cr_lo; // ri = sqrt(q) * cr  (cr = dnu/df = dt/du) as fp32 pair
+  float vpi;          // V / pi (fp32)
+  float inv_rows2;    // 1 / (2 V)
+  float img_scale;    // amplitude_scale / L^2
+  float ss_weight;    // span / A (slant stack)
+  float ss_inv_dt;    // 1 / dt
+  const float2* tw_L;   // [L]   exp(-2 pi i j / L)
+  const float2* tw_np;  // [npad]
+  const float* ramp_g;  // [npad] 2 pi |f| taper / npad
+  const float* omb;     // [n_t]  1 - bump
+  const float* bump_s;  // [S]    bump over the support
+  const float2* psi;    // [H]    exp(2 pi i f_k) / den_k
+  const float2* rho;    // [H]    ref_k / den_k
+  const float2* modt;   // [L]    half-node modulation (or null)
+  const float4* angtab; // [V/4+3] (cos_hi, cos_lo, sin_hi, sin_lo) of u*pi/V
+  const double2* ss_cs; // [A]    (cos, sin) of the input angles
+};
+
+struct Work {
+  float2* polar;
+  float* rowcoef;
+  float* part;
+  float2* common;
+  float* coefmean;
+  float2* columns;
+  float* filtered;
+  int* status;  // [0] non-finite input, [1] non-finite output
+  int groups;   // K1 CTAs per slice (partial-sum groups)
+  int pairs_per_cta;
+};
+
+template <int L>
+struct KShape {
+  using S = FftShape<L>;
+  static constexpr int RPT = S::RPT;
+  static constexpr int TPF = S::TPF;
+  static constexpr int THREADS = TPF < 32 ? 32 : TPF;
+  // smem buffer (float2) for the FFT passes and the K1 Z_k / Z_{L-k} exchange
+  static constexpr int BUF = S::SMEM > 0 ? S::SMEM : L;
+};
+
+// ---------------------------------------------------------------------------
+// K1: radial kernel (fused ramp when npad == L)
+// ---------------------------------------------------------------------------
+template <int L, bool RAMP>
+__global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
+  using K = KShape<L>;
+  constexpr int RPT = K::RPT, TPF = K::TPF;
+  extern __shared__ float2 smem[];
+  float2* buf = smem;
+  float* sacc = reinterpret_cast<float*>(smem + K::BUF);
+  const int t = threadIdx.x;
+  const bool active = t < TPF;
+  const int q = blockIdx.y;
+  const int g = blockIdx.x;
+  const int npairs = (p.rows + 1) >> 1;
+  const int pr_begin = g * w.pairs_per_cta;
+  const int pr_end = min(npairs, pr_begin + w.pairs_per_cta);
+  const int H = L / 2;
+
+  for (int i = t; i < p.S; i += blockDim.x) sacc[i] = 0.f;
+  __syncthreads();
+  bool bad = false;
+
+  for (int pr = pr_begin; pr < pr_end; ++pr) {
+    const int j0 = 2 * pr, j1 = 2 * pr + 1;
+    const bool has1 = j1 < p.rows;
+    const float* y0 = sino + ((size_t)q * p.rows + j0) * p.n_t;
+    const float* y1 = y0 + p.n_t;
+    float2 v[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int idx = t + i * TPF;
+      float a = 0.f, b = 0.f;
+      if (active && idx < p.n_t) {
+        a = __ldg(y0 + idx);
+        if (has1) b = __ldg(y1 + idx);
+        bad |= !isfinite(a) || !isfinite(b);
+      }
+      v[i] = make_float2(a, b);
+    }
+    if constexpr (RAMP) {
+      fft<L, false>(v, buf, t, active, p.tw_np);
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const float gk = active ? __ldg(p.ramp_g + t + i * TPF) : 0.f;
+        v[i] = cscale(v[i], gk);
+      }
+      fft<L, true>(v, buf, t, active, p.tw_np);
+    }
+    // v[i] = (h_j0, h_j1)(t_idx) for idx < n_t: support sums, window, zero pad
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int idx = t + i * TPF;
+      if (active) {
+        const int s = idx - p.lo;
+        if (s >= 0 && s < p.S) sacc[s] += v[i].x + v[i].y;
+        const float m = idx < p.n_t ? __ldg(p.omb + idx) : 0.f;
+        v[i] = cscale(v[i], m);
+      }
+    }
+    fft<L, false>(v, buf, t, active, p.tw_L);
+    // exchange Z_k / Z_{L-k} through smem to separate the two real rows
+    if constexpr (FftShape<L>::SMEM > 0) {
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) buf[spad(t + i * TPF)] = v[i];
+      }
+    } else {
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) buf[t + i * TPF] = v[i];
+      }
+    }
+    __syncthreads();
+    const float2 z0 = buf[0];
+    const float a0 = z0.x * p.inv_nt, a1 = z0.y * p.inv_nt;
+    float2* out0 = w.polar + ((size_t)q * p.rows + j0) * H;
+    float2* out1 = out0 + H;
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int k = t + i * TPF;
+        if (k < H) {
+          const int km = (L - k) & (L - 1);
+          const float2 zk = v[i];
+          const float2 zm = buf[FftShape<L>::SMEM > 0 ? spad(km) : km];
+          const float2 X = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+          const float2 Y = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+          const float2 ps = __ldg(p.psi + k), rh = __ldg(p.rho + k);
+          float2 A0 = cmul(ps, X), A1 = cmul(ps, Y);
+          A0 = make_float2(fmaf(-a0, rh.x, A0.x), fmaf(-a0, rh.y, A0.y));
+          A1 = make_float2(fmaf(-a1, rh.x, A1.x), fmaf(-a1, rh.y, A1.y));
+          if (k == 0) { A0 = make_float2(0.f, 0.f); A1 = A0; }
+          out0[k] = A0;
+          if (has1) out1[k] = A1;
+        }
+      }
+    }
+    if (t == 0) {
+      w.rowcoef[(size_t)q * p.rows + j0] = a0;
+      if (has1) w.rowcoef[(size_t)q * p.rows + j1] = a1;
+    }
+    __syncthreads();
+  }
+  if (bad) atomicOr(&w.status[0], 1);
+  float* part = w.part + ((size_t)q * w.groups + g) * p.S;
+  for (int i = t; i < p.S; i += blockDim.x) part[i] = sacc[i];
+}
+
+// ---------------------------------------------------------------------------
+// KR: standalone ramp filter (rows -> rows), fourier_bp.py:469-505
+// ---------------------------------------------------------------------------
+template <int NP>
+__global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const float* __restrict__ sino,
+                                                               float* __restrict__ out, int total_rows, Work w) {
+  using K = KShape<NP>;
+  constexpr int RPT = K::RPT, TPF = K::TPF;
+  extern __shared__ float2 smem[];
+  const int t = threadIdx.x;
+  const bool active = t < TPF;
+  const int j0 = 2 * blockIdx.x, j1 = j0 + 1;
+  const bool has1 = j1 < total_rows;
+  const float* y0 = sino + (size_t)j0 * p.n_t;
+  const float* y1 = y0 + p.n_t;
+  float2 v[RPT];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int idx = t + i * TPF;
+    float a = 0.f, b = 0.f;
+    if (active && idx < p.n_t) {
+      a = __ldg(y0 + idx);
+      if (has1) b = __ldg(y1 + idx);
+      bad |= !isfinite(a) || !isfinite(b);
+    }
+    v[i] = make_float2(a, b);
+  }
+  fft<NP, false>(v, smem, t, active, p.tw_np);
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const float gk = active ? __ldg(p.ramp_g + t + i * TPF) : 0.f;
+    v[i] = cscale(v[i], gk);
+  }
+  fft<NP, true>(v, smem, t, active, p.tw_np);
+  if (active) {
+    float* o0 = out + (size_t)j0 * p.n_t;
+    float* o1 = o0 + p.n_t;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int idx = t + i * TPF;
+      if (idx < p.n_t) {
+        o0[idx] = v[i].x;
+        if (has1) o1[idx] = v[i].y;
+      }
+    }
+  }
+  if (bad && w.status) atomicOr(&w.status[0], 1);
+}
+
+// ---------------------------------------------------------------------------
+// K1b: common (angle-independent) row and coef.mean() per slice
+// ---------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(KShape<L>::THREADS) k1b_common(DevPlan p, Work w) {
+  using K = KShape<L>;
+  constexpr int RPT = K::RPT, TPF = K::TPF;
+  constexpr int H = L / 2;
+  extern __shared__ float2 smem[];
+  float2* buf = smem;
+  float* cs = reinterpret_cast<float*>(smem + K::BUF);
+  float* bm = cs + p.S;
+  float* red = bm + p.S;  // [blockDim]
+  const int t = threadIdx.x;
+  const bool active = t < TPF;
+  const int q = blockIdx.x;
+  const float* part = w.part + (size_t)q * w.groups * p.S;
+  for (int i = t; i < p.S; i += blockDim.x) {
+    float s = 0.f;
+    for (int g = 0; g < w.groups; ++g) s += part[(size_t)g * p.S + i];
+    cs[i] = s;
+  }
+  __syncthreads();
+  float csum = 0.f;
+  for (int i = t; i < p.S; i += blockDim.x) {
+    const float m = (p.full_turn ? cs[i] : cs[i] + cs[p.S - 1 - i]) * p.inv_rows2;
+    const float b = __ldg(p.bump_s + i) * m;
+    bm[i] = b;
+    csum += b;
+  }
+  // rect coefficient of the common row and mean of the per-row coefficients
+  float asum = 0.f;
+  for (int j = t; j < p.rows; j += blockDim.x) asum += w.rowcoef[(size_t)q * p.rows + j];
+  red[t] = csum;
+  red[t + blockDim.x] = asum;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (t < s) {
+      red[t] += red[t + s];
+      red[t + blockDim.x] += red[t + s + blockDim.x];
+    }
+    __syncthreads();
+  }
+  const float c = red[0] * p.inv_nt;
+  const float amean = red[blockDim.x] / (float)p.rows;
+  float2 v[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int idx = t + i * TPF;
+    const int s = idx - p.lo;
+    v[i] = make_float2((active && s >= 0 && s < p.S) ? bm[s] : 0.f, 0.f);
+  }
+  __syncthreads();
+  fft<L, false>(v, buf, t, active, p.tw_L);
+  if (active) {
+    float2* out = w.common + (size_t)q * H;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int k = t + i * TPF;
+      if (k < H) {
+        const float2 ps = __ldg(p.psi + k), rh = __ldg(p.rho + k);
+        float2 C = cmul(ps, v[i]);
+        C = make_float2(fmaf(-c, rh.x, C.x), fmaf(-c, rh.y, C.y));
+        if (k == 0) C = make_float2(0.f, 0.f);
+        out[k] = C;
+      }
+    }
+  }
+  if (t == 0) w.coefmean[q] = amean + c;
+}
+
+// ---------------------------------------------------------------------------
+// gridding coordinates (fourier_bp.py:226-247) in compensated fp32
+// ---------------------------------------------------------------------------
+struct NodeCoord {
+  int r0;    // floor(ri)
+  float rf;  // ri - r0 in [0, 1)
+  int t0;    // floor(ti) mod 2V
+  float tf;  // ti - floor(ti)
+};
+
+// ri = hypot(a, b) * dnu / df ; ti = (atan2(b, a) mod 2 pi) * V / pi
+__device__ __forceinline__ NodeCoord node_coord(const DevPlan& p, int as, int bs) {
+  NodeCoord c;
+  const int q = as * as + bs * bs;
+  if (q == 0) {
+    c.r0 = 0; c.rf = 0.f; c.t0 = 0; c.tf = 0.f;
+    return c;
+  }
+  // --- radius: sqrt(q) as (sh + sl), times (cr_hi + cr_lo)
+  {
+    const float qh = (float)q;
+    const float ql = (float)(q - (int)qh);
+    const float sh = sqrtf(qh);
+    const float e = fmaf(-sh, sh, qh) + ql;
+    const float sl = e * (0.5f / sh);
+    const float ph = sh * p.cr_hi;
+    const float pe = fmaf(sh, p.cr_hi, -ph);
+    const float plo = pe + fmaf(sh, p.cr_lo, sl * p.cr_hi);
+    float r0 = floorf(ph);
+    float rf = (ph - r0) + plo;
+    if (rf < 0.f) { rf += 1.f; r0 -= 1.f; }
+    else if (rf >= 1.f) { rf -= 1.f; r0 += 1.f; }
+    c.r0 = (int)r0;
+    c.rf = rf;
+  }
+  // --- angle: octant reduction + residual against the tabulated angle
+  {
+    const int ax = abs(as), ay = abs(bs);
+    const bool sw = ay > ax;
+    const float mx = (float)(sw ? ay : ax);
+    const float mn = (float)(sw ? ax : ay);
+    const float ue = atanf(__fdividef(mn, mx)) * p.vpi;  // estimate, u in [0, V/4]
+    int ui = (int)ue;
+    const float4 cs = __ldg(p.angtab + ui);                // cos/sin(ui*pi/V) hi/lo
+    const float p1 = mn * cs.x, e1 = fmaf(mn, cs.x, -p1);
+    const float p2 = mx * cs.z, e2 = fmaf(mx, cs.z, -p2);
+    const float num = (p1 - p2) + ((e1 - e2) + fmaf(mn, cs.y, -mx * cs.w));
+    const float den = fmaf(mx, cs.x, mn * cs.z);
+    float uf = atanf(num / den) * p.vpi;
+    if (uf < 0.f) { uf += 1.f; ui -= 1; }
+    else if (uf >= 1.f) { uf -= 1.f; ui += 1; }
+    // quadrant angle in half-index units: tq = sw ? V/2 - u : u
+    int tq2;     // 2 * integer part contribution
+    float sf;    // signed fraction
+    if (sw) { tq2 = p.n_theta - 2 * ui; sf = -uf; }
+    else { tq2 = 2 * ui; sf = uf; }
+    // full angle: ti = base + s * tq
+    int base2, s;
+    if (as >= 0) {
+      if (bs >= 0) { base2 = 0; s = 1; }
+      else { base2 = 4 * p.n_theta; s = -1; }
+    } else {
+      if (bs >= 0) { base2 = 2 * p.n_theta; s = -1; }
+      else { base2 = 2 * p.n_theta; s = 1; }
+    }
+    const int I2 = base2 + s * tq2;
+    float fr = (float)s * sf;
+    int I;
+    if (I2 & 1) { I = (I2 - 1) >> 1; fr += 0.5f; }
+    else { I = I2 >> 1; }
+    if (fr < 0.f) { fr += 1.f; I -= 1; }
+    else if (fr >= 1.f) { fr -= 1.f; I += 1; }
+    const int rows2 = 2 * p.n_theta;
+    I %= rows2;
+    if (I < 0) I += rows2;
+    c.t0 = I;
+    c.tf = fr;
+  }
+  return c;
+}
+
+// polar sample P(t, r) of the full circle: mirror rows are conjugates for
+// half-turn input (fourier_bp.py:302-311; SURVEY.md finding 2)
+__device__ __forceinline__ float2 polar_at(const DevPlan& p, const float2* __restrict__ pol, int t, int r) {
+  if (p.full_turn) return __ldg(pol + (size_t)t * p.H + r);
+  if (t < p.n_theta) return __ldg(pol + (size_t)t * p.H + r);
+  const float2 v = __ldg(pol + (size_t)(t - p.n_theta) * p.H + r);
+  return make_float2(v.x, -v.y);
+}
+
+// interpolated, modulated lattice value C(as, bs) (fourier_bp.py:389-407, 427-430)
+__device__ __forceinline__ float2 lattice_value(const DevPlan& p, const float2* __restrict__ pol,
+                                                const float2* __restrict__ com, int as, int bs) {
+  const NodeCoord c = node_coord(p, as, bs);
+  const int top = p.H - 1;
+  const int rows2 = 2 * p.n_theta;
+  float2 val;
+  if (p.interp == 0) {
+    if (c.r0 > top || (c.r0 == top && c.rf > 0.f)) return make_float2(0.f, 0.f);
+    const int ra = min(c.r0, top), rb = min(c.r0 + 1, top);
+    const int t1 = c.t0 + 1 == rows2 ? 0 : c.t0 + 1;
+    const float2 p00 = polar_at(p, pol, c.t0, ra), p01 = polar_at(p, pol, c.t0, rb);
+    const float2 p10 = polar_at(p, pol, t1, ra), p11 = polar_at(p, pol, t1, rb);
+    const float2 c0 = __ldg(com + ra), c1 = __ldg(com + rb);
+    const float rf = c.rf, tf = c.tf;
+    const float2 r0v = make_float2(fmaf(rf, p01.x - p00.x, p00.x), fmaf(rf, p01.y - p00.y, p00.y));
+    const float2 r1v = make_float2(fmaf(rf, p11.x - p10.x, p10.x), fmaf(rf, p11.y - p10.y, p10.y));
+    const float2 cv = make_float2(fmaf(rf, c1.x - c0.x, c0.x), fmaf(rf, c1.y - c0.y, c0.y));
+    val = make_float2(fmaf(tf, r1v.x - r0v.x, r0v.x) + cv.x, fmaf(tf, r1v.y - r0v.y, r0v.y) + cv.y);
+  } else {
+    // nearest: np.rint (half to even) on both coordinates (fourier_bp.py:234-238)
+    int ir = c.r0 + ((c.rf > 0.5f || (c.rf == 0.5f && (c.r0 & 1))) ? 1 : 0);
+    if (ir > top) return make_float2(0.f, 0.f);
+    int it = c.t0 + ((c.tf > 0.5f || (c.tf == 0.5f && (c.t0 & 1))) ? 1 : 0);
+    if (it >= rows2) it -= rows2;
+    const float2 pv = polar_at(p, pol, it, ir);
+    const float2 cv = __ldg(com + ir);
+    val = make_float2(pv.x + cv.x, pv.y + cv.y);
+  }
+  if (p.has_mod) {
+    const int L = p.L;
+    val = cmul(val, cmul(__ldg(p.modt + (as & (L - 1))), __ldg(p.modt + (bs & (L - 1)))));
+  }
+  return val;
+}
+
+// ---------------------------------------------------------------------------
+// K2: gather + IFFT along k2 for one Cartesian column a in [0, H]
+// ---------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work w) {
+  using K = KShape<L>;
+  constexpr int RPT = K::RPT, TPF = K::TPF;
+  constexpr int H = L / 2;
+  extern __shared__ float2 smem[];
+  const int t = threadIdx.x;
+  const bool active = t < TPF;
+  const int a = blockIdx.x;
+  const int q = blockIdx.y;
+  const int as = a < H ? a : -H;
+  const float2* pol = w.polar + (size_t)q * p.rows * H;
+  const float2* com = w.common + (size_t)q * H;
+  float2 v[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    float2 val = make_float2(0.f, 0.f);
+    if (active) {
+      const int b = t + i * TPF;
+      const int bs = b < H ? b : b - L;
+      val = lattice_value(p, pol, com, as, bs);
+      // Hermitian part: 0.5 (C[k] + conj C[-k mod L]) (.real of ifft2, fourier_bp.py:431)
+      if (p.full_turn || (p.nyq && (a == H || b == H))) {
+        const int pa = as == -H ? -H : -as;
+        const int pb = bs == -H ? -H : -bs;
+        const float2 m = lattice_value(p, pol, com, pa, pb);
+        val = make_float2(0.5f * (val.x + m.x), 0.5f * (val.y - m.y));
+      }
+    }
+    v[i] = val;
+  }
+  fft<L, true>(v, smem, t, active, p.tw_L);
+  if (active) {
+    float2* out = w.columns + ((size_t)q * (H + 1) + a) * p.n;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int idx = t + i * TPF;
+      const int m2 = (idx + p.n_half) & (L - 1);
+      if (m2 < p.n) out[m2] = v[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: C2R along k1 for a pair of output rows + epilogue
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float coverage(float x1, float x2) {
+  // fourier_bp.py:204-220 : pi inside the unit circle, 2 asin(1/r) outside
+  const float r = sqrtf(fmaf(x1, x1, x2 * x2));
+  return r > 1.f ? 2.f * asinf(1.f / r) : 3.14159265358979323846f;
+}
+
+template <int L>
+__global__ void __launch_bounds__(KShape<L>::THREADS) k3_rows(DevPlan p, Work w, float* __restrict__ img,
+                                                              float out_scale) {
+  using K = KShape<L>;
+  constexpr int RPT = K::RPT, TPF = K::TPF;
+  constexpr int H = L / 2;
+  extern __shared__ float2 smem[];
+  const int t = threadIdx.x;
+  const bool active = t < TPF;
+  const int m2a = 2 * blockIdx.x, m2b = m2a + 1;
+  const int q = blockIdx.y;
+  const int n = p.n;
+  const bool hasb = m2b < n;
+  const float2* G = w.columns + (size_t)q * (H + 1) * n;
+  float2 v[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    float2 z = make_float2(0.f, 0.f);
+    if (active) {
+      const int a = t + i * TPF;
+      const int ar = a <= H ? a : L - a;
+      const float2* row = G + (size_t)ar * n;
+      float2 ga = __ldg(row + m2a);
+      float2 gb = hasb ? __ldg(row + m2b) : make_float2(0.f, 0.f);
+      if (a == 0 || a == H) { ga.y = 0.f; gb.y = 0.f; }
+      if (a > H) { ga.y = -ga.y; gb.y = -gb.y; }
+      z = make_float2(ga.x - gb.y, ga.y + gb.x);  // ga + i gb
+    }
+    v[i] = z;
+  }
+  fft<L, true>(v, smem, t, active, p.tw_L);
+  bool bad = false;
+  if (active) {
+    const float cm = w.coefmean[q];
+    const float inv_n = 2.f / (float)n;
+    const float x2a = -1.f + ((float)m2a + 0.5f) * inv_n;
+    const float x2b = -1.f + ((float)m2b + 0.5f) * inv_n;
+    float* oa = img + ((size_t)q * n + m2a) * n;
+    float* ob = oa + n;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int idx = t + i * TPF;
+      const int m1 = (idx + p.n_half) & (L - 1);
+      if (m1 < n) {
+        const float x1 = -1.f + ((float)m1 + 0.5f) * inv_n;
+        const float ra = fmaf(v[i].x, p.img_scale, cm * coverage(x1, x2a)) * out_scale;
+        oa[m1] = ra;
+        bad |= !isfinite(ra);
+        if (hasb) {
+          const float rb = fmaf(v[i].y, p.img_scale, cm * coverage(x1, x2b)) * out_scale;
+          ob[m1] = rb;
+          bad |= !isfinite(rb);
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(&w.status[1], 1);
+}
+
+// ---------------------------------------------------------------------------
+// K5: slant-stack backprojection (projector.py:126-158)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k5_slant(DevPlan p, const float* __restrict__ rows, int n_ang,
+                                                float* __restrict__ img, float scale, Work w) {
+  const int m1 = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int m2 = blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int q = blockIdx.z;
+  const int n = p.n;
+  if (m1 >= n || m2 >= n) return;
+  const double x = -1.0 + 2.0 * ((double)m1 + 0.5) / (double)n;
+  const double y = -1.0 + 2.0 * ((double)m2 + 0.5) / (double)n;
+  const float* base = rows + (size_t)q * n_ang * p.n_t;
+  const double top = (double)(p.n_t - 1);
+  const double inv_dt = (double)p.ss_inv_dt;
+  float acc = 0.f;
+  for (int j = 0; j < n_ang; ++j) {
+    const double2 cs = __ldg(p.ss_cs + j);
+    const double fi = (fma(x, cs.x, y * cs.y) + 1.0) * inv_dt;
+    if (fi >= 0.0 && fi <= top) {
+      const double fl = floor(fi);
+      const float fr = (float)(fi - fl);
+      int i0 = (int)fl;
+      i0 = min(max(i0, 0), p.n_t - 2);
+      const float* r = base + (size_t)j * p.n_t + i0;
+      const float r0 = __ldg(r), r1 = __ldg(r + 1);
+      acc += fmaf(fr, r1 - r0, r0);
+    }
+  }
+  const float out = acc * p.ss_weight * scale;
+  img[((size_t)q * n + m2) * n + m1] = out;
+  if (w.status && !isfinite(out)) atomicOr(&w.status[1], 1);
+}
+
+}  // namespace tb

@@ -1,0 +1,212 @@
+"""GPU parity: the sm_100a path against the reference's golden outputs and
+the CPU oracle.  Tolerances follow BASELINE.json north_star: relative L2
+<= 1e-4 and max-abs <= 1e-3 * max|ref| (float32 compute vs float64 reference)."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from golden_util import GOLDEN_DIR, load_case, oracle_plan, rel_l2, max_rel  # noqa: E402
+from oracle import bst_oracle as O  # noqa: E402
+
+REL_L2_TOL = 1e-4
+MAX_ABS_TOL = 1e-3
+
+CASES = sorted(f[:-4] for f in os.listdir(GOLDEN_DIR) if f.endswith(".npz"))
+
+
+def _F():
+    from paper_1704_08364_b200 import fourier_bp as F
+    return F
+
+
+def _plans(case):
+    F = _F()
+    p = case["params"]
+    n_ang, n_t = case["sino"].shape
+    plan = F.BstPlan(n_t=n_t, n_theta=p["n_theta"], **p["plan"])
+    fplan = F.FilterPlan(**p["filter"])
+    return plan, fplan
+
+
+def _sino(case):
+    from paper_1704_08364_b200.grids import AngleAxis, DetectorAxis, Sinogram
+    s = case["sino"]
+    ft = case["params"]["full_turn"]
+    return Sinogram(DetectorAxis(s.shape[1]), AngleAxis(s.shape[0], full_turn=ft), s.astype(np.float64))
+
+
+def _assert_close(got, ref, rel=REL_L2_TOL, mx=MAX_ABS_TOL):
+    r, m = rel_l2(got, ref), max_rel(got, ref)
+    assert r <= rel and m <= mx, f"rel_l2={r:.3e} max_abs/max={m:.3e}"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fbp_bst_matches_reference_golden(name):
+    c = load_case(name)
+    plan, fplan = _plans(c)
+    got = _F().fbp(_sino(c), plan, fplan, kernel="bst").data
+    _assert_close(got, c["fbp_bst"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_bst_backproject_matches_reference_golden(name):
+    c = load_case(name)
+    plan, _ = _plans(c)
+    got = _F().bst_backproject(_sino(c), plan).data
+    _assert_close(got, c["bst"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_ramp_filter_matches_reference_golden(name):
+    c = load_case(name)
+    _, fplan = _plans(c)
+    got = _F().ramp_filter(_sino(c), fplan).data
+    _assert_close(got, c["ramp"], rel=1e-5, mx=1e-5)
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if "fbp_ss" in np.load(os.path.join(GOLDEN_DIR, n + ".npz")).files])
+def test_fbp_ss_matches_reference_golden(name):
+    c = load_case(name)
+    plan, fplan = _plans(c)
+    got = _F().fbp(_sino(c), plan, fplan, kernel="ss").data
+    _assert_close(got, c["fbp_ss"])
+
+
+# --- per-kernel checks through the workspace --------------------------------
+
+@pytest.mark.parametrize("name", ["shepp256", "white300x180", "outn128", "fullturn128", "odd65x33_n63"])
+def test_each_kernel_against_three_kernel_oracle(name):
+    F = _F()
+    c = load_case(name)
+    plan, fplan = _plans(c)
+    op = oracle_plan(c)
+    ft = c["params"]["full_turn"]
+    nat = F.native_plan(plan, fplan, ft, 0)
+    sino = torch.from_numpy(c["sino"]).cuda()
+    img = torch.empty((plan.output_n, plan.output_n), device="cuda")
+    ws = nat.new_workspace(1)
+    nat.reset_status(ws)
+    nat.run("fbp", sino, img, 1, 1, ws)
+    nat.read_status(ws)
+    lay = nat.layout(1)
+    H, rows, n = nat.L // 2, nat.n_angles, nat.n
+
+    def view(off, count, dtype):
+        b = ws[off: off + count * torch.tensor([], dtype=dtype).element_size()]
+        return b.view(dtype).cpu().numpy()
+
+    h = O.ramp_filter(c["sino"].astype(np.float64), op)
+    Ahat, a, colsum = O.k1_polar(h, op)
+    Chat, coef_mean = O.k1b_common(colsum, a, op, ft)
+    G = O.k2_columns(Ahat, Chat, op, ft)
+    pol = view(lay["polar"], rows * H * 2, torch.float32).view(np.complex64).reshape(rows, H)
+    assert rel_l2(pol, Ahat) < 2e-5
+    rc = view(lay["rowcoef"], rows, torch.float32)
+    assert np.max(np.abs(rc - a)) <= 1e-5 * np.max(np.abs(a)) + 1e-7
+    com = view(lay["common"], H * 2, torch.float32).view(np.complex64)
+    assert np.linalg.norm(com - Chat) <= 2e-5 * np.linalg.norm(Chat) + 1e-6 * np.linalg.norm(Ahat) / np.sqrt(rows)
+    cm = view(lay["coefmean"], 1, torch.float32)[0]
+    assert abs(cm - coef_mean) <= 1e-5 * max(1.0, abs(coef_mean))
+    cols = view(lay["columns"], (H + 1) * n * 2, torch.float32).view(np.complex64).reshape(H + 1, n)
+    assert rel_l2(cols, G) < 5e-5
+
+
+# --- larger sizes against the oracle -----------------------------------------
+
+@pytest.mark.parametrize("size,noise", [(512, 0.05), (1024, 0.05), (2048, 0.05)])
+def test_large_slice_against_oracle(size, noise):
+    F = _F()
+    from paper_1704_08364_b200.grids import AngleAxis, DetectorAxis, Sinogram
+    rng = np.random.default_rng(0)
+    s = O.ellipse_sinogram([(1.0, 0.5, 0.4, 0.1, -0.05, 0.0)], size, size)
+    s = (s + rng.normal(0.0, noise, s.shape)).astype(np.float32)
+    y = Sinogram(DetectorAxis(size), AngleAxis(size), s.astype(np.float64))
+    got = F.fbp(y, F.BstPlan(size, size)).data
+    ref = O.fbp(s.astype(np.float64), O.OraclePlan(size, size))
+    _assert_close(got, ref)
+
+
+def test_white_noise_2048_against_oracle():
+    F = _F()
+    from paper_1704_08364_b200.grids import AngleAxis, DetectorAxis, Sinogram
+    s = np.random.default_rng(1).normal(0.0, 1.0, (2048, 2048)).astype(np.float32)
+    y = Sinogram(DetectorAxis(2048), AngleAxis(2048), s.astype(np.float64))
+    got = F.fbp(y, F.BstPlan(2048, 2048)).data
+    ref = O.fbp(s.astype(np.float64), O.OraclePlan(2048, 2048))
+    _assert_close(got, ref)
+
+
+# --- volume API ---------------------------------------------------------------
+
+def test_volume_matches_per_slice_and_is_batch_invariant():
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    vol = phantom.ellipsoid_volume(10, 256, 256, device="cuda")
+    vol += 0.01 * torch.randn(vol.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
+    plan = F.BstPlan(256, 256)
+    a = F.fbp_volume(vol, plan, batch=1)
+    b = F.fbp_volume(vol, plan, batch=3)
+    c = F.fbp_volume(vol, plan, batch=10)
+    assert torch.equal(a, b) and torch.equal(a, c)  # slices are independent: bitwise
+    host = vol.cpu().numpy().astype(np.float64)
+    for k in (0, 4, 9):
+        ref = O.fbp(host[k], O.OraclePlan(256, 256))
+        _assert_close(a[k].cpu().numpy(), ref)
+
+
+def test_host_volume_pipeline_equals_device_path():
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    vol = phantom.ellipsoid_volume(37, 128, 96, device="cuda")
+    plan = F.BstPlan(128, 96)
+    dev = F.fbp_volume(vol, plan, batch=4)
+    host = F.fbp_volume(vol.cpu(), plan, batch=4, chunk=8, devices=[0])
+    assert not host.is_cuda
+    assert torch.equal(dev.cpu(), host)
+
+
+def test_volume_nonfinite_input_raises():
+    F = _F()
+    vol = torch.zeros((3, 64, 64), device="cuda")
+    vol[1, 5, 7] = float("nan")
+    with pytest.raises(ValueError):
+        F.fbp_volume(vol, F.BstPlan(64, 64))
+
+
+def test_full_size_properties_2048():
+    """Size-independent properties at the benchmark shape: linearity and the
+    constant-sinogram identity (BST gives pi*c exactly)."""
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    plan = F.BstPlan(2048, 2048)
+    x = phantom.ellipsoid_volume(2, 2048, 2048, device="cuda")
+    g = torch.Generator("cuda").manual_seed(3)
+    z = torch.randn(x.shape, device="cuda", generator=g)
+    fx = F.fbp_volume(x, plan)
+    fz = F.fbp_volume(z, plan)
+    fxz = F.fbp_volume(2.0 * x - 0.5 * z, plan)
+    lin = torch.linalg.norm(fxz - (2.0 * fx - 0.5 * fz)) / torch.linalg.norm(fxz)
+    assert lin.item() < 1e-5
+    const = torch.full((1, 2048, 2048), 0.75, device="cuda")
+    b = F.fbp_volume(const, plan, kernel="none")[0].cpu().numpy()
+    expect = 0.75 * O.OraclePlan(2048, 2048).coverage()  # pi inside |u| <= 1, 2 asin(1/r) outside
+    assert np.max(np.abs(b - expect)) <= 2e-5 * np.pi * 0.75
+
+
+def test_determinism_repeat_bitwise():
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    x = phantom.ellipsoid_volume(4, 512, 512, device="cuda")
+    plan = F.BstPlan(512, 512)
+    assert torch.equal(F.fbp_volume(x, plan), F.fbp_volume(x, plan))
