@@ -160,7 +160,7 @@ struct FftShape {
 
 // One Stockham pass.  tw[j] = exp(-2 pi i j / N) for j < N (fp32).
 template <int N, int PASS, bool INV>
-__device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* buf, int t,
+__device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
                                          const float2* __restrict__ tw) {
   using S = FftShape<N>;
   constexpr int R = S::radix(PASS);
@@ -175,7 +175,7 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
 #pragma unroll
     for (int m = 0; m < R; ++m) {
       if constexpr (FIRST) x[b][m] = v[b + m * PER];
-      else x[b][m] = buf[spad(t + b * S::TPF + m * NB)];
+      else x[b][m] = active ? buf[spad(t + b * S::TPF + m * NB)] : make_float2(0.f, 0.f);
     }
   if constexpr (!FIRST) __syncthreads();
 #pragma unroll
@@ -183,7 +183,7 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
     const int j = t + b * S::TPF;
     const int k = j & (NS - 1);
     if constexpr (NS > 1) {
-      float2 w = __ldg(&tw[k * (N / (NS * R))]);
+      float2 w = active ? __ldg(&tw[k * (N / (NS * R))]) : make_float2(1.f, 0.f);
       if (INV) w.y = -w.y;
       float2 wp[R];
       wp[1] = w;
@@ -196,7 +196,7 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
     if constexpr (LAST) {
 #pragma unroll
       for (int m = 0; m < R; ++m) v[b + m * PER] = x[b][m];
-    } else {
+    } else if (active) {
       const int base = (j / NS) * NS * R + k;
 #pragma unroll
       for (int m = 0; m < R; ++m) buf[spad(base + m * NS)] = x[b][m];
@@ -209,21 +209,16 @@ template <int N, bool INV, int PASS = 0>
 __device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
                                            const float2* __restrict__ tw) {
   if constexpr (PASS < FftShape<N>::NPASS) {
-    constexpr bool LAST = PASS == FftShape<N>::NPASS - 1;
-    constexpr bool FIRST = PASS == 0;
-    if (active) {
-      fft_pass<N, PASS, INV>(v, buf, t, tw);
-    } else {
-      // keep the CTA-wide barriers balanced for idle threads
-      if constexpr (!FIRST) __syncthreads();
-      if constexpr (!LAST) __syncthreads();
-    }
+    // every thread runs the same instruction stream (bar.sync is .aligned:
+    // no barrier may sit under a thread-divergent branch); idle threads only
+    // mask their shared-memory and table traffic
+    fft_pass<N, PASS, INV>(v, buf, t, active, tw);
     fft_passes<N, INV, PASS + 1>(v, buf, t, active, tw);
   }
 }
 
 // Full transform.  Must be called by every thread of the CTA (barriers);
-// threads with !active only take part in the barriers.  On return the
+// threads with !active compute on zeros and touch no memory.  On return the
 // buffer may be reused only after a __syncthreads().
 template <int N, bool INV>
 __device__ __forceinline__ void fft(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,

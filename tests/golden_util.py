@@ -23,9 +23,14 @@ def oracle_plan(case):
     return OraclePlan(n_t=n_t, n_theta=p["n_theta"], rolloff=roll, **p["plan"])
 
 
+def _wide(a):
+    a = np.asarray(a)
+    return a.astype(np.complex128 if np.iscomplexobj(a) else np.float64)
+
+
 def rel_l2(a, b):
-    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+    return float(np.linalg.norm(_wide(a) - b) / np.linalg.norm(b))
 
 
 def max_rel(a, b):
-    return float(np.max(np.abs(np.asarray(a, np.float64) - b)) / np.max(np.abs(b)))
+    return float(np.max(np.abs(_wide(a) - b)) / np.max(np.abs(b)))
