@@ -1,0 +1,344 @@
+"""Benchmark: 2048^3 BST filtered backprojection (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--size 2048] [--impl ours|reference]
+
+One "step" reconstructs the whole synthetic 2048^3 sinogram volume
+(V = n_t = 2048 angles x detector samples per slice, 2048 slices, n = 2048
+output) -- configs[3] of BASELINE.json, which fits one B200.  Under torchrun
+(N > 1) the volume is slab-sharded over the ranks (contiguous z-slabs, no
+data-path collective; a barrier and a MAX all-reduce of the timings only):
+total work is fixed, so scaling is "strong".
+
+value       voxels/s of the whole job, inputs resident in HBM, CUDA events on
+            the launching stream around K steps, max over ranks.
+e2e         the same metric through the public API `fbp_volume` with pinned
+            HOST input/output: H2D, compute and D2H inside the timed region.
+roofline    dominant kernel: algorithmic bytes per launch (SURVEY.md 8d:
+            K1 = 4 V n_t + 8 V H, K2 = 8 V H + 8 (H+1) n, K3 = 8 (H+1) n + 4 n^2
+            per slice) / its average CUDA-event launch time, against the
+            measured HBM copy bandwidth in MEASURED_PEAKS.json.
+cpu_baseline  the CPU oracle restatement of the reference (oracle/bst_oracle.py,
+            kind "port") on a bounded slice sample using all host cores.
+
+`--impl reference` times that CPU reference restatement alone on the host
+(rank 0 only) and prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2048^3 volume recon seconds & voxels/s at 1/2/4/8 B200; % HBM roofline"
+UNIT = "voxels/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--size", type=int, default=2048, help="N for the N^3 workload (V = n_t = n = N)")
+    ap.add_argument("--batch", type=int, default=None, help="slices per launch group")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-slices", type=int, default=None)
+    return ap.parse_args()
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _workload(n):
+    return {"workload": f"{n}^3 BST FBP: {n} slices x {n} angles x {n} detector -> {n}^3 image, fp32",
+            "n_slices": n, "n_angles": n, "n_t": n, "output_n": n}
+
+
+def _algorithmic_bytes(V, n_t, L, n):
+    H = L // 2
+    k1 = 4 * V * n_t + 8 * V * H
+    k2 = 8 * V * H + 8 * (H + 1) * n
+    k3 = 8 * (H + 1) * n + 4 * n * n
+    return {"k1_radial": k1, "k2_columns": k2, "k3_rows": k3, "total": k1 + k2 + k3}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) timing
+# ---------------------------------------------------------------------------
+
+def _cpu_sample(n, slices, threads):
+    """Time the oracle restatement of the reference on `slices` slices of the
+    n^3 workload with a `threads`-wide pool (the reference pipeline's
+    backproject-stage workers); returns (seconds, voxels/s)."""
+    import numpy as np
+    from oracle import bst_oracle as O
+    plan = O.OraclePlan(n, n)
+    first = n // 2 - slices // 2
+    vol = O.ellipsoid_volume_sinogram(n, n, n, slices=(first, first + slices))
+    vol = vol.astype(np.float32).astype(np.float64)
+    O.fbp(vol[0], plan)  # warm caches / allocator outside the clock
+    t0 = time.perf_counter()
+    O.fbp_volume(vol, plan, workers=threads)
+    dt = time.perf_counter() - t0
+    return dt, slices * n * n / dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.size
+    threads = os.cpu_count() or 1
+    slices = args.cpu_slices or max(threads, 4)
+    for _ in range(args.warmup):
+        _cpu_sample(n, min(slices, threads), threads)
+    times, rates = [], []
+    for _ in range(args.steps):
+        dt, r = _cpu_sample(n, slices, threads)
+        times.append(dt)
+        rates.append(r)
+    value = statistics.median(rates)
+    sample = f"{slices} of {n} slices of the {n}^3 workload per step (oracle fbp_volume, {threads} threads), extrapolated"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * (n ** 3) / value, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic ellipsoid phantom)",
+        "config": _workload(n),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1704_08364_b200 import fourier_bp as F
+    from paper_1704_08364_b200 import phantom
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = args.size
+    plan = F.BstPlan(n, n)
+    slabs = F._split(n, world)
+    b, e = slabs[rank]
+    S = e - b
+    batch = args.batch or F.default_batch(plan)
+
+    # synthetic input: per-slice analytic ellipsoid sinogram of this rank's slab
+    sino = phantom.ellipsoid_volume(n, n, n, device=dev, chunk=32, slices=(b, e))
+    img = torch.empty((S, n, n), dtype=torch.float32, device=dev)
+    nat = F.native_plan(plan, F.FilterPlan(), False, local)
+    ws = nat.new_workspace(batch)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        nat.run("fbp", sino, img, S, batch, ws, stream)
+
+    nat.reset_status(ws)
+    for _ in range(args.warmup):
+        step()
+    nat.read_status(ws)
+
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms_total / args.steps
+    value = (n ** 3) / (ms_step / 1e3)
+
+    # per-kernel device times on the same workload (one extra profiled step)
+    torch.cuda.synchronize()
+    stage = nat.run_profiled(sino, img, S, batch, ws, stream)
+    launches = {"k1_radial": math.ceil(S / batch), "k1b_common": math.ceil(S / batch),
+                "k2_columns": math.ceil(S / batch), "k3_rows": math.ceil(S / batch)}
+    alg = _algorithmic_bytes(n, n, plan.radial_samples, n)
+    dom = max(("k1_radial", "k2_columns", "k3_rows"), key=lambda k: stage[k])
+    per_launch_ms = stage[dom] / launches[dom]
+    slices_per_launch = S / launches[dom]
+    achieved = alg[dom] * slices_per_launch / (per_launch_ms / 1e3) / 1e9
+    peak, peak_src = _peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("kernel") == dom and tr.get("size") == n:
+            traffic = tr["dram_bytes_per_slice"] * slices_per_launch
+    except Exception:
+        pass
+    nat.read_status(ws)
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty((S, n, n), dtype=torch.float32, pin_memory=True)
+        host_in.copy_(sino)
+        host_out = torch.empty((S, n, n), dtype=torch.float32, pin_memory=True)
+        del img
+        torch.cuda.empty_cache()
+        F.fbp_volume(host_in, plan, out=host_out, devices=[local], batch=batch)  # warm-up
+        k = args.e2e_steps or max(1, min(args.steps, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            F.fbp_volume(host_in, plan, out=host_out, devices=[local], batch=batch)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / k)
+        e2e = {"value": (n ** 3) / e2e_s, "unit": UNIT, "s_per_step": e2e_s,
+               "h2d_bytes_per_step": S * n * n * 4, "d2h_bytes_per_step": S * n * n * 4}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        slices = args.cpu_slices or max(threads, 4)
+        dt, rate = _cpu_sample(n, slices, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{slices} of {n} slices of the {n}^3 workload (oracle fbp_volume, {threads} threads, "
+                         f"{dt:.1f} s), extrapolated"}
+
+    if rank == 0:
+        cfg = _workload(n)
+        cfg.update({"batch": batch, "slab_slices_per_rank": S, "parallelism": f"slab{world}",
+                    "l2": "inputs larger than L2 (32 GiB sinogram volume streamed per step)"})
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "seconds_per_volume": ms_step / 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (analytic off-centre ellipsoid sinograms, generated on device)",
+            "config": cfg,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_slice": alg[dom]},
+            "path_roofline": {"algorithmic_bytes_per_volume": alg["total"] * n,
+                              "achieved_gbs": alg["total"] * n / (ms_step / 1e3) / 1e9 / world,
+                              "frac_per_gpu": alg["total"] * n / (ms_step / 1e3) / 1e9 / world / peak},
+            "stage_ms_per_step": {k: v for k, v in stage.items() if v > 0},
+            "gpu_launches": sum(launches.values()) * args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

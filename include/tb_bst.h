@@ -110,6 +110,13 @@ int tb_workspace_get_layout(const tb_plan* plan, int batch, tb_workspace_layout*
 int tb_fbp(const tb_plan* plan, const float* sino, float* image, int n_slices,
            int batch, void* workspace, size_t workspace_bytes, void* stream);
 
+/* tb_fbp with CUDA events around every kernel launch (measurement only):
+ * synchronises `stream` and adds each stage's summed device time in ms to
+ * stage_ms[5] = {ramp (unfused path), K1, K1b, K2, K3}. */
+int tb_fbp_profiled(const tb_plan* plan, const float* sino, float* image, int n_slices,
+                    int batch, void* workspace, size_t workspace_bytes, void* stream,
+                    double* stage_ms);
+
 /* BST backprojection only (input already ramp-filtered; no 1/(2 pi)). */
 int tb_bst(const tb_plan* plan, const float* sino, float* image, int n_slices,
            int batch, void* workspace, size_t workspace_bytes, void* stream);

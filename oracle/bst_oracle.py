@@ -68,6 +68,12 @@ class OraclePlan:
     output_n: int | None = None
     rolloff: float = 1.0  # FilterPlan.effective_rolloff (fourier_bp.py:265-267)
 
+    def _memo(self, key, build):
+        cache = self.__dict__.setdefault("_tables", {})
+        if key not in cache:
+            cache[key] = build()
+        return cache[key]
+
     def __post_init__(self):
         # validation mirrors fourier_bp.py:88-109
         if self.n_t < 2 or self.n_theta < 1:
@@ -134,38 +140,38 @@ class OraclePlan:
     def amp(self) -> float:
         return (self.dnu * self.L) ** 2 * self.dt
 
-    # tables (fourier_bp.py:164-220)
+    # tables (fourier_bp.py:164-220), built once per plan like the reference's cache
     def t_samples(self) -> np.ndarray:
         return -1.0 + 2.0 * np.arange(self.n_t) / (self.n_t - 1)  # grids.py:61-62
 
-    def freqs(self) -> np.ndarray:
+    def _build_freqs(self) -> np.ndarray:
         return np.fft.fftfreq(self.L, d=self.dt)
 
-    def phase(self) -> np.ndarray:
+    def _build_phase(self) -> np.ndarray:
         return np.exp(2j * np.pi * self.freqs() * (1.0 - self.roll * self.dt))
 
-    def bump(self) -> np.ndarray:
+    def _build_bump(self) -> np.ndarray:
         t = self.t_samples()
         arg = np.sqrt(np.maximum(1.0 - (t / self.kb_support) ** 2, 0.0))
         val = _i0(self.kb_beta * arg) / _i0(self.kb_beta)
         return np.where(np.abs(t) <= self.kb_support, val, 0.0)
 
-    def ref_spectrum(self) -> np.ndarray:
+    def _build_ref_spectrum(self) -> np.ndarray:
         ones = np.zeros(self.L)
         ones[: self.n_t] = 1.0
         return np.fft.fft(np.roll(ones, -self.roll)) * self.phase()
 
-    def denom(self) -> np.ndarray:
+    def _build_denom(self) -> np.ndarray:
         return np.maximum(np.abs(self.freqs()), self.sigma_min)
 
-    def coverage(self) -> np.ndarray:
+    def _build_coverage(self) -> np.ndarray:
         x = -1.0 + 2.0 * (np.arange(self.n) + 0.5) / self.n
         r = np.sqrt(x[None, :] ** 2 + x[:, None] ** 2)
         with np.errstate(divide="ignore", invalid="ignore"):
             far = 2.0 * np.arcsin(np.minimum(1.0, 1.0 / np.maximum(r, 1e-300)))
         return np.where(r > 1.0, far, np.pi)
 
-    def modulation(self) -> np.ndarray | None:
+    def _build_modulation(self) -> np.ndarray | None:
         """Half-node shift of inverse_dft2_and_shift (fourier_bp.py:424-430)."""
         L, n = self.L, self.n
         m0 = L // 2 - n // 2
@@ -175,7 +181,7 @@ class OraclePlan:
         nu = np.fft.fftfreq(L) * L * self.dnu
         return np.exp(2j * np.pi * nu * delta)
 
-    def lattice_coords(self):
+    def _build_lattice_coords(self):
         """(ri, ti) of every Cartesian node, rows <-> nu2, cols <-> nu1
         (fourier_bp.py:226-232)."""
         L = self.L
@@ -184,6 +190,30 @@ class OraclePlan:
         ang = np.mod(np.arctan2(nu[:, None], nu[None, :]), 2.0 * np.pi)
         ti = ang * (2 * self.n_theta / (2.0 * np.pi))
         return ri, ti
+
+    def freqs(self):
+        return self._memo('freqs', self._build_freqs)
+
+    def phase(self):
+        return self._memo('phase', self._build_phase)
+
+    def bump(self):
+        return self._memo('bump', self._build_bump)
+
+    def ref_spectrum(self):
+        return self._memo('ref_spectrum', self._build_ref_spectrum)
+
+    def denom(self):
+        return self._memo('denom', self._build_denom)
+
+    def coverage(self):
+        return self._memo('coverage', self._build_coverage)
+
+    def modulation(self):
+        return self._memo('modulation', self._build_modulation)
+
+    def lattice_coords(self):
+        return self._memo('lattice_coords', self._build_lattice_coords)
 
 
 # ---------------------------------------------------------------------------
@@ -525,15 +555,18 @@ def ellipse_sinogram(ellipses, n_t: int, n_angles: int, full_turn: bool = False)
 
 
 def ellipsoid_volume_sinogram(n_slices: int, n_t: int, n_angles: int,
-                              a=0.5, b=0.4, c=0.5, center=(0.1, -0.05, 0.0), rho=1.0) -> np.ndarray:
+                              a=0.5, b=0.4, c=0.5, center=(0.1, -0.05, 0.0), rho=1.0,
+                              slices: tuple[int, int] | None = None) -> np.ndarray:
     """Per-slice analytic sinogram of one off-centre ellipsoid at slice heights
-    s_k = -1 + 2(k+1/2)/S (cli.py:156, phantom.py:44-50, 67-93)."""
-    vol = np.zeros((n_slices, n_angles, n_t))
-    for k in range(n_slices):
+    s_k = -1 + 2(k+1/2)/S (cli.py:156, phantom.py:44-50, 67-93); ``slices``
+    restricts to the slab [b, e)."""
+    first, last = slices if slices is not None else (0, n_slices)
+    vol = np.zeros((last - first, n_angles, n_t))
+    for k in range(first, last):
         s = -1.0 + 2.0 * (k + 0.5) / n_slices
         srel = (s - center[2]) / c
         if abs(srel) > 1.0:
             continue
         sc = math.sqrt(max(1.0 - srel * srel, 0.0))
-        vol[k] = ellipse_sinogram([(rho, a * sc, b * sc, center[0], center[1], 0.0)], n_t, n_angles)
+        vol[k - first] = ellipse_sinogram([(rho, a * sc, b * sc, center[0], center[1], 0.0)], n_t, n_angles)
     return vol

@@ -84,6 +84,7 @@ def _bind(lib):
         "tb_workspace_get_layout": (I, [P, I, ctypes.POINTER(tb_workspace_layout)]),
         "tb_fbp": (I, [P, P, P, I, I, P, S, P]),
         "tb_bst": (I, [P, P, P, I, I, P, S, P]),
+        "tb_fbp_profiled": (I, [P, P, P, I, I, P, S, P, ctypes.POINTER(ctypes.c_double)]),
         "tb_ramp": (I, [P, P, P, I, P]),
         "tb_ss": (I, [P, P, P, I, ctypes.c_float, P]),
         "tb_fbp_ss": (I, [P, P, P, I, I, P, S, P]),

@@ -135,29 +135,44 @@ struct Launch {
     return TB_OK;
   }
 
-  // one launch group of B slices through K1 -> K1b -> K2 -> K3
+  // one launch group of B slices through K1 -> K1b -> K2 -> K3.  `ev`, when
+  // given, receives start/stop events around each stage: [stage][2] with
+  // stages 0 ramp (unfused path), 1 K1, 2 K1b, 3 K2, 4 K3.
   static int bst_group(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp,
-                       float out_scale, cudaStream_t st) {
+                       float out_scale, cudaStream_t st, cudaEvent_t* ev) {
     const DevPlan& dp = p->dp;
     const float* k1_in = sino;
     bool fused = false;
+    auto mark = [&](int stage, int which) {
+      if (ev) cudaEventRecord(ev[2 * stage + which], st);
+    };
     if (ramp) {
       if (p->npad == L) {
         fused = true;
       } else {
+        mark(0, 0);
         int rc = ramp_rows(p, sino, w.filtered, B * p->rows, w, st);
+        mark(0, 1);
         if (rc) return rc;
         k1_in = w.filtered;
       }
     }
     dim3 g1(p->groups, B);
+    mark(1, 0);
     if (fused)
       tb::k1_radial<L, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
     else
       tb::k1_radial<L, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    mark(1, 1);
+    mark(2, 0);
     tb::k1b_common<L><<<B, K::THREADS, smem_k1b(p), st>>>(dp, w);
+    mark(2, 1);
+    mark(3, 0);
     tb::k2_columns<L><<<dim3(p->H + 1, B), K::THREADS, smem_fft(), st>>>(dp, w);
+    mark(3, 1);
+    mark(4, 0);
     tb::k3_rows<L><<<dim3((p->n + 1) / 2, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
+    mark(4, 1);
     TB_CUDA(cudaGetLastError());
     return TB_OK;
   }
@@ -212,8 +227,8 @@ int Launch<L>::ramp_rows(const tb_plan* p, const float* in, float* out, int tota
 int configure_dispatch(const tb_plan* p) { TB_DISPATCH_L(p->L, Launch<L_>::configure(p)) }
 
 int bst_dispatch(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp, float scale,
-                 cudaStream_t st) {
-  TB_DISPATCH_L(p->L, Launch<L_>::bst_group(p, sino, img, B, w, ramp, scale, st))
+                 cudaStream_t st, cudaEvent_t* ev = nullptr) {
+  TB_DISPATCH_L(p->L, Launch<L_>::bst_group(p, sino, img, B, w, ramp, scale, st, ev))
 }
 
 int check_exec_args(const tb_plan* p, const void* a, const void* b, int n_slices, int batch, const void* ws,
@@ -241,20 +256,44 @@ int set_device(const tb_plan* p) {
 }
 
 int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, int batch, void* ws,
-                 size_t ws_bytes, void* stream, bool ramp, float scale) {
+                 size_t ws_bytes, void* stream, bool ramp, float scale, double* stage_ms = nullptr) {
   int rc = check_exec_args(p, sino, img, n_slices, batch, ws, ws_bytes);
   if (rc) return rc;
   if ((rc = set_device(p))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t in_stride = (size_t)p->rows * p->n_t;
   const size_t out_stride = (size_t)p->n * p->n;
-  for (int s0 = 0; s0 < n_slices; s0 += batch) {
+  const int ngroups = (n_slices + batch - 1) / batch;
+  std::vector<cudaEvent_t> evs;
+  if (stage_ms) {
+    for (int i = 0; i < 5; ++i) stage_ms[i] = 0.0;
+    evs.resize((size_t)ngroups * 10);
+    for (auto& e : evs) TB_CUDA(cudaEventCreate(&e));
+  }
+  for (int g = 0; g < ngroups; ++g) {
+    const int s0 = g * batch;
     const int B = std::min(batch, n_slices - s0);
     Work w = work_for(p, batch, ws);
-    rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, st);
-    if (rc) return rc;
+    rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, st,
+                      stage_ms ? evs.data() + (size_t)g * 10 : nullptr);
+    if (rc) break;
   }
-  return TB_OK;
+  if (stage_ms) {
+    if (!rc) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = fail(TB_ERR_CUDA, cudaGetErrorString(e));
+    }
+    const bool unfused = ramp && p->npad != p->L;
+    for (int g = 0; g < ngroups && !rc; ++g)
+      for (int k = 0; k < 5; ++k) {
+        if (k == 0 && !unfused) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, evs[(size_t)g * 10 + 2 * k], evs[(size_t)g * 10 + 2 * k + 1]) == cudaSuccess)
+          stage_ms[k] += ms;
+      }
+    for (auto& e : evs) cudaEventDestroy(e);
+  }
+  return rc;
 }
 
 }  // namespace
@@ -584,6 +623,13 @@ int tb_workspace_get_layout(const tb_plan* p, int batch, tb_workspace_layout* ou
 int tb_fbp(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws, size_t ws_bytes,
            void* stream) {
   return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)));
+}
+
+int tb_fbp_profiled(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws,
+                    size_t ws_bytes, void* stream, double* stage_ms) {
+  if (!stage_ms) return fail(TB_ERR_INVALID, "null stage_ms");
+  return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)),
+                      stage_ms);
 }
 
 int tb_bst(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws, size_t ws_bytes,

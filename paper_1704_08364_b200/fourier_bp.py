@@ -232,6 +232,16 @@ class NativePlan:
                 self._stream(stream))
         _native.check(rc, f"tb_{op}")
 
+    def run_profiled(self, sino: torch.Tensor, image: torch.Tensor, n_slices: int, batch: int,
+                     workspace: torch.Tensor, stream=None) -> dict:
+        """tb_fbp with per-stage CUDA events; returns summed device ms per stage."""
+        ms = (ctypes.c_double * 5)()
+        rc = self._lib.tb_fbp_profiled(self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(image.data_ptr()),
+                                       int(n_slices), int(batch), ctypes.c_void_p(workspace.data_ptr()),
+                                       ctypes.c_size_t(workspace.numel()), self._stream(stream), ms)
+        _native.check(rc, "tb_fbp_profiled")
+        return dict(zip(("ramp", "k1_radial", "k1b_common", "k2_columns", "k3_rows"), list(ms)))
+
     def ramp(self, sino: torch.Tensor, out: torch.Tensor, n_slices: int, stream=None) -> None:
         rc = self._lib.tb_ramp(self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                int(n_slices), self._stream(stream))

@@ -51,17 +51,20 @@ def ellipses_sinogram(ellipses, n_t: int, n_angles: int, full_turn: bool = False
 
 
 def ellipsoid_volume(n_slices: int, n_t: int, n_angles: int, a=0.5, b=0.4, c=0.5, center=(0.1, -0.05, 0.0),
-                     rho=1.0, device="cpu", out: torch.Tensor | None = None, chunk: int = 64) -> torch.Tensor:
+                     rho=1.0, device="cpu", out: torch.Tensor | None = None, chunk: int = 64,
+                     slices: tuple[int, int] | None = None) -> torch.Tensor:
     """float32 [S][A][n_t] sinogram volume of one off-centre ellipsoid sliced
-    at s_k = -1 + 2(k + 1/2)/S (cli.py:156; phantom.py:44-50, 67-93)."""
+    at s_k = -1 + 2(k + 1/2)/S (cli.py:156; phantom.py:44-50, 67-93).
+    ``slices=(b, e)`` generates only the slab k in [b, e)."""
+    first, last = slices if slices is not None else (0, n_slices)
     if out is None:
-        out = torch.empty((n_slices, n_angles, n_t), dtype=torch.float32, device=device)
+        out = torch.empty((last - first, n_angles, n_t), dtype=torch.float32, device=device)
     t, th = _grids(n_t, n_angles, False, out.device)
     cos_t, sin_t = torch.cos(th), torch.sin(th)
     shift = (center[0] * cos_t + center[1] * sin_t)[:, None]
     tp2 = (t[None, :] - shift) ** 2
-    for k0 in range(0, n_slices, chunk):
-        k1 = min(n_slices, k0 + chunk)
+    for k0 in range(first, last, chunk):
+        k1 = min(last, k0 + chunk)
         s = -1.0 + 2.0 * (torch.arange(k0, k1, dtype=torch.float64, device=out.device) + 0.5) / n_slices
         srel = (s - center[2]) / c
         scale = torch.sqrt(torch.clamp(1.0 - srel * srel, min=0.0))
@@ -70,5 +73,5 @@ def ellipsoid_volume(n_slices: int, n_t: int, n_angles: int, a=0.5, b=0.4, c=0.5
         under = torch.clamp(q2[:, :, None] - tp2[None], min=0.0)
         val = 2.0 * rho * (as_ * bs)[:, None, None] * torch.sqrt(under) / torch.clamp(q2, min=1e-300)[:, :, None]
         val = torch.where((srel.abs() <= 1.0)[:, None, None], val, torch.zeros_like(val))
-        out[k0:k1].copy_(val.to(torch.float32))
+        out[k0 - first:k1 - first].copy_(val.to(torch.float32))
     return out
