@@ -67,13 +67,17 @@ struct tb_plan {
   double amp;
   int groups, pairs_per_cta;
   DevPlan dp;
-  void* blob = nullptr;  // all device tables in one allocation
+  void* blob = nullptr;   // all small device tables in one allocation
+  void* table = nullptr;  // gridding table [(H+1)^2] uint2
 };
 
 namespace {
 
+constexpr int kLanes = 2;  // concurrent launch groups (streams) per call
+
 struct Layout {
   size_t polar, rowcoef, part, common, coefmean, columns, filtered, status, total;
+  size_t lane_bytes;  // stride between the per-lane regions (all but status)
 };
 
 Layout layout_for(const tb_plan* p, int B) {
@@ -90,15 +94,16 @@ Layout layout_for(const tb_plan* p, int B) {
   l.part = take((size_t)B * p->groups * std::max(p->S, 1) * sizeof(float));
   l.common = take((size_t)B * p->H * sizeof(float2));
   l.coefmean = take((size_t)B * sizeof(float));
-  l.columns = take((size_t)B * (p->H + 1) * p->n * sizeof(float2));
+  l.columns = take((size_t)B * p->dp.col_slice * sizeof(float2));
   l.filtered = take((size_t)B * p->rows * p->n_t * sizeof(float));
-  l.total = off;
+  l.lane_bytes = off - l.polar;
+  l.total = off + (kLanes - 1) * l.lane_bytes;
   return l;
 }
 
-Work work_for(const tb_plan* p, int B, void* ws) {
+Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   Layout l = layout_for(p, B);
-  char* base = static_cast<char*>(ws);
+  char* base = static_cast<char*>(ws) + (size_t)lane * l.lane_bytes;
   Work w;
   w.polar = reinterpret_cast<float2*>(base + l.polar);
   w.rowcoef = reinterpret_cast<float*>(base + l.rowcoef);
@@ -107,7 +112,7 @@ Work work_for(const tb_plan* p, int B, void* ws) {
   w.coefmean = reinterpret_cast<float*>(base + l.coefmean);
   w.columns = reinterpret_cast<float2*>(base + l.columns);
   w.filtered = reinterpret_cast<float*>(base + l.filtered);
-  w.status = reinterpret_cast<int*>(base + l.status);
+  w.status = reinterpret_cast<int*>(static_cast<char*>(ws) + l.status);
   w.groups = p->groups;
   w.pairs_per_cta = p->pairs_per_cta;
   return w;
@@ -121,7 +126,7 @@ struct Launch {
   using K = tb::KShape<L>;
   static size_t smem_k1(const tb_plan* p) { return K::BUF * sizeof(float2) + (size_t)std::max(p->S, 1) * 4; }
   static size_t smem_k1b(const tb_plan* p) {
-    return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::THREADS * 4;
+    return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::K1B_THREADS * 4;
   }
   static size_t smem_fft() { return K::BUF * sizeof(float2); }
 
@@ -129,8 +134,12 @@ struct Launch {
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
-    TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    if constexpr (L >= 64) {
+      TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+      TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    }
     TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     return TB_OK;
   }
@@ -165,13 +174,20 @@ struct Launch {
       tb::k1_radial<L, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
     mark(1, 1);
     mark(2, 0);
-    tb::k1b_common<L><<<B, K::THREADS, smem_k1b(p), st>>>(dp, w);
+    tb::k1b_common<L><<<B, K::K1B_THREADS, smem_k1b(p), st>>>(dp, w);
     mark(2, 1);
+    const bool half = L >= 64 && 2 * p->n == L;
     mark(3, 0);
-    tb::k2_columns<L><<<dim3(p->H + 1, B), K::THREADS, smem_fft(), st>>>(dp, w);
+    if (half)
+      tb::k2_columns<L, (L >= 64)><<<dim3(p->H + 1, B), K::THREADS, smem_fft(), st>>>(dp, w);
+    else
+      tb::k2_columns<L, false><<<dim3(p->H + 1, B), K::THREADS, smem_fft(), st>>>(dp, w);
     mark(3, 1);
     mark(4, 0);
-    tb::k3_rows<L><<<dim3((p->n + 1) / 2, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
+    if (half)
+      tb::k3_rows<L, (L >= 64)><<<dim3((p->n + 3) / 4, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
+    else
+      tb::k3_rows<L, false><<<dim3((p->n + 3) / 4, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
     mark(4, 1);
     TB_CUDA(cudaGetLastError());
     return TB_OK;
@@ -270,13 +286,35 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
     evs.resize((size_t)ngroups * 10);
     for (auto& e : evs) TB_CUDA(cudaEventCreate(&e));
   }
+  // two lanes: launch group g runs on lane g % 2 (the caller's stream and an
+  // auxiliary stream forked from it), each lane with its own workspace region,
+  // so one group's serial K1b / kernel tails overlap the other group's work.
+  // The profiled variant stays on one lane so per-kernel times are clean.
+  const int lanes = (stage_ms || ngroups < 2) ? 1 : kLanes;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (lanes > 1) {
+    TB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    TB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    TB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    TB_CUDA(cudaEventRecord(fork, st));
+    TB_CUDA(cudaStreamWaitEvent(aux, fork, 0));
+  }
   for (int g = 0; g < ngroups; ++g) {
     const int s0 = g * batch;
     const int B = std::min(batch, n_slices - s0);
-    Work w = work_for(p, batch, ws);
-    rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, st,
+    const int lane = g % lanes;
+    Work w = work_for(p, batch, ws, lane);
+    rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, lane ? aux : st,
                       stage_ms ? evs.data() + (size_t)g * 10 : nullptr);
     if (rc) break;
+  }
+  if (lanes > 1) {
+    cudaEventRecord(join, aux);
+    cudaStreamWaitEvent(st, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    cudaStreamDestroy(aux);  // released once its queued work completes
   }
   if (stage_ms) {
     if (!rc) {
@@ -378,9 +416,9 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   p->hi = hi;
   p->S = hi - lo + 1;
 
-  // --- K1 work split: <= 128 CTAs (partial-sum groups) per slice
+  // --- K1 work split: <= 256 CTAs (partial-sum groups) per slice
   const int npairs = (p->rows + 1) / 2;
-  p->pairs_per_cta = std::max(1, (npairs + 127) / 128);
+  p->pairs_per_cta = std::max(1, (npairs + 255) / 256);
   p->groups = (npairs + p->pairs_per_cta - 1) / p->pairs_per_cta;
 
   // --- host tables
@@ -461,15 +499,6 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
       }
     }
   }
-  // tabulated angles u * pi / V for the octant-reduced residual (double-float)
-  const int nang = V / 4 + 3;
-  std::vector<float4> angtab(nang);
-  for (int u = 0; u < nang; ++u) {
-    const double th = (double)u * kPi / V;
-    const double c = std::cos(th), s = std::sin(th);
-    const float ch = (float)c, sh = (float)s;
-    angtab[u] = make_float4(ch, (float)(c - ch), sh, (float)(s - sh));
-  }
   // slant-stack angles (grids.py:85-95; projector.py:137-141)
   const int A = p->rows;
   const double span = d->full_turn ? 2.0 * kPi : kPi;
@@ -494,7 +523,6 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   const size_t o_psi = take(psi.size() * sizeof(float2));
   const size_t o_rho = take(rho.size() * sizeof(float2));
   const size_t o_mod = take(modt.size() * sizeof(float2));
-  const size_t o_ang = take(angtab.size() * sizeof(float4));
   const size_t o_ss = take(sscs.size() * sizeof(double2));
   std::vector<char> host(off, 0);
   auto put = [&](size_t o, const void* src, size_t bytes) { std::memcpy(host.data() + o, src, bytes); };
@@ -506,13 +534,13 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   put(o_psi, psi.data(), psi.size() * sizeof(float2));
   put(o_rho, rho.data(), rho.size() * sizeof(float2));
   put(o_mod, modt.data(), modt.size() * sizeof(float2));
-  put(o_ang, angtab.data(), angtab.size() * sizeof(float4));
   put(o_ss, sscs.data(), sscs.size() * sizeof(double2));
 
   int prev = -1;
   cudaGetDevice(&prev);
   auto cleanup = [&](int code, const std::string& msg) {
     if (p->blob) cudaFree(p->blob);
+    if (p->table) cudaFree(p->table);
     delete p;
     if (prev >= 0) cudaSetDevice(prev);
     return fail(code, msg);
@@ -543,9 +571,6 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   dp.has_mod = has_mod;
   dp.n_half = n / 2;
   dp.inv_nt = (float)(1.0 / n_t);
-  dp.cr_hi = (float)cr;
-  dp.cr_lo = (float)(cr - (double)dp.cr_hi);
-  dp.vpi = (float)(V / kPi);
   dp.inv_rows2 = (float)(1.0 / (2.0 * V));
   dp.img_scale = (float)(p->amp / ((double)L * (double)L));
   dp.ss_weight = (float)(span / A);
@@ -558,8 +583,21 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   dp.psi = reinterpret_cast<const float2*>(b + o_psi);
   dp.rho = reinterpret_cast<const float2*>(b + o_rho);
   dp.modt = reinterpret_cast<const float2*>(b + o_mod);
-  dp.angtab = reinterpret_cast<const float4*>(b + o_ang);
+  dp.col_slice = (size_t)((n + 3) / 4) * (H + 1) * 4;
   dp.ss_cs = reinterpret_cast<const double2*>(b + o_ss);
+
+  // gridding table (fourier_bp.py:222-249), built on the device in fp64
+  if ((long long)V / 2 >= 65535) return cleanup(TB_ERR_UNSUPPORTED, "n_theta too large for the gridding table");
+  {
+    const long long cnt = (long long)(H + 1) * (H + 1);
+    e = cudaMalloc(&p->table, cnt * sizeof(uint2));
+    if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc(table): ") + cudaGetErrorString(e));
+    tb::build_grid_table<<<(unsigned)((cnt + 255) / 256), 256>>>(static_cast<uint2*>(p->table), H, dnu, df,
+                                                                  (2.0 * V) / (2.0 * kPi), d->interp);
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("build_grid_table: ") + cudaGetErrorString(e));
+    dp.gridtab = static_cast<const uint2*>(p->table);
+  }
 
   int rc = configure_dispatch(p);
   if (rc) {
@@ -578,6 +616,7 @@ int tb_plan_destroy(tb_plan* p) {
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
     cudaFree(p->blob);
+    if (p->table) cudaFree(p->table);
     if (prev >= 0) cudaSetDevice(prev);
   }
   delete p;

@@ -18,7 +18,7 @@
 //   polar   [B][rows][H]       rows = processed angles = A, H = L/2 radial bins
 //   part    [B][groups][S]     per-CTA partial column sums over the KB support
 //   rowcoef [B][rows], common [B][H], coefmean [B]
-//   columns [B][H+1][n]        K2 output, k1-major
+//   columns [B][ceil(n/4)][H+1][4]  K2 output in 4-row tiles (k1-major inside a tile)
 //   image   [B][n][n]
 #pragma once
 #include "fft.cuh"
@@ -32,8 +32,6 @@ struct DevPlan {
   int has_mod;
   int n_half;         // n/2 (crop offset)
   float inv_nt;
-  float cr_hi, cr_lo; // ri = sqrt(q) * cr  (cr = dnu/df = dt/du) as fp32 pair
-  float vpi;          // V / pi (fp32)
   float inv_rows2;    // 1 / (2 V)
   float img_scale;    // amplitude_scale / L^2
   float ss_weight;    // span / A (slant stack)
@@ -46,8 +44,9 @@ struct DevPlan {
   const float2* psi;    // [H]    exp(2 pi i f_k) / den_k
   const float2* rho;    // [H]    ref_k / den_k
   const float2* modt;   // [L]    half-node modulation (or null)
-  const float4* angtab; // [V/4+3] (cos_hi, cos_lo, sin_hi, sin_lo) of u*pi/V
   const double2* ss_cs; // [A]    (cos, sin) of the input angles
+  const uint2* gridtab; // [(H+1)^2] first-quadrant gridding table
+  size_t col_slice;     // complex elements per slice of the K2 output (tiled)
 };
 
 struct Work {
@@ -71,6 +70,7 @@ struct KShape {
   static constexpr int THREADS = TPF < 32 ? 32 : TPF;
   // smem buffer (float2) for the FFT passes and the K1 Z_k / Z_{L-k} exchange
   static constexpr int BUF = S::SMEM > 0 ? S::SMEM : L;
+  static constexpr int K1B_THREADS = THREADS < 512 ? 512 : THREADS;
 };
 
 // ---------------------------------------------------------------------------
@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const
     for (int i = 0; i < RPT; ++i) {
       const int idx = t + i * TPF;
       float a = 0.f, b = 0.f;
-      if (active && idx < p.n_t) {
+      // n_t <= L/2 always (L >= pad_factor * n_t, pad_factor >= 2): the upper
+      // half of every padded row is a compile-time zero (pruned first pass)
+      if (i < RPT / 2 && active && idx < p.n_t) {
         a = __ldg(y0 + idx);
         if (has1) b = __ldg(y1 + idx);
         bad |= !isfinite(a) || !isfinite(b);
@@ -126,7 +128,9 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int idx = t + i * TPF;
-      if (active) {
+      if (i >= RPT / 2) {
+        v[i] = make_float2(0.f, 0.f);  // crop to n_t + zero pad: outputs i >= RPT/2 are dead
+      } else if (active) {
         const int s = idx - p.lo;
         if (s >= 0 && s < p.S) sacc[s] += v[i].x + v[i].y;
         const float m = idx < p.n_t ? __ldg(p.omb + idx) : 0.f;
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const 
 // K1b: common (angle-independent) row and coef.mean() per slice
 // ---------------------------------------------------------------------------
 template <int L>
-__global__ void __launch_bounds__(KShape<L>::THREADS) k1b_common(DevPlan p, Work w) {
+__global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, Work w) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   constexpr int H = L / 2;
@@ -304,119 +308,91 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k1b_common(DevPlan p, Work
 }
 
 // ---------------------------------------------------------------------------
-// gridding coordinates (fourier_bp.py:226-247) in compensated fp32
+// gridding table (fourier_bp.py:222-249): built once per plan in fp64.
+// One entry per first-quadrant lattice node (|a|, |b|) in [0, H]^2, stored
+// [|a|][|b|] so a Cartesian column reads it contiguously:
+//   x = r0 (16 bits, 0xFFFF = outside the disc) | floor(tq) << 16
+//   y = unorm16 frac(ri) | unorm16 frac(tq) << 16
+// with ri = hypot(nu1, nu2)/df and tq = atan2(|nu2|, |nu1|) * 2V / (2 pi).
+// The quantised fractions carry <= 2^-17 absolute weight error.
 // ---------------------------------------------------------------------------
-struct NodeCoord {
-  int r0;    // floor(ri)
-  float rf;  // ri - r0 in [0, 1)
-  int t0;    // floor(ti) mod 2V
-  float tf;  // ti - floor(ti)
-};
-
-// ri = hypot(a, b) * dnu / df ; ti = (atan2(b, a) mod 2 pi) * V / pi
-__device__ __forceinline__ NodeCoord node_coord(const DevPlan& p, int as, int bs) {
-  NodeCoord c;
-  const int q = as * as + bs * bs;
-  if (q == 0) {
-    c.r0 = 0; c.rf = 0.f; c.t0 = 0; c.tf = 0.f;
-    return c;
-  }
-  // --- radius: sqrt(q) as (sh + sl), times (cr_hi + cr_lo)
-  {
-    const float qh = (float)q;
-    const float ql = (float)(q - (int)qh);
-    const float sh = sqrtf(qh);
-    const float e = fmaf(-sh, sh, qh) + ql;
-    const float sl = e * (0.5f / sh);
-    const float ph = sh * p.cr_hi;
-    const float pe = fmaf(sh, p.cr_hi, -ph);
-    const float plo = pe + fmaf(sh, p.cr_lo, sl * p.cr_hi);
-    float r0 = floorf(ph);
-    float rf = (ph - r0) + plo;
-    if (rf < 0.f) { rf += 1.f; r0 -= 1.f; }
-    else if (rf >= 1.f) { rf -= 1.f; r0 += 1.f; }
-    c.r0 = (int)r0;
-    c.rf = rf;
-  }
-  // --- angle: octant reduction + residual against the tabulated angle
-  {
-    const int ax = abs(as), ay = abs(bs);
-    const bool sw = ay > ax;
-    const float mx = (float)(sw ? ay : ax);
-    const float mn = (float)(sw ? ax : ay);
-    const float ue = atanf(__fdividef(mn, mx)) * p.vpi;  // estimate, u in [0, V/4]
-    int ui = (int)ue;
-    const float4 cs = __ldg(p.angtab + ui);                // cos/sin(ui*pi/V) hi/lo
-    const float p1 = mn * cs.x, e1 = fmaf(mn, cs.x, -p1);
-    const float p2 = mx * cs.z, e2 = fmaf(mx, cs.z, -p2);
-    const float num = (p1 - p2) + ((e1 - e2) + fmaf(mn, cs.y, -mx * cs.w));
-    const float den = fmaf(mx, cs.x, mn * cs.z);
-    float uf = atanf(num / den) * p.vpi;
-    if (uf < 0.f) { uf += 1.f; ui -= 1; }
-    else if (uf >= 1.f) { uf -= 1.f; ui += 1; }
-    // quadrant angle in half-index units: tq = sw ? V/2 - u : u
-    int tq2;     // 2 * integer part contribution
-    float sf;    // signed fraction
-    if (sw) { tq2 = p.n_theta - 2 * ui; sf = -uf; }
-    else { tq2 = 2 * ui; sf = uf; }
-    // full angle: ti = base + s * tq
-    int base2, s;
-    if (as >= 0) {
-      if (bs >= 0) { base2 = 0; s = 1; }
-      else { base2 = 4 * p.n_theta; s = -1; }
-    } else {
-      if (bs >= 0) { base2 = 2 * p.n_theta; s = -1; }
-      else { base2 = 2 * p.n_theta; s = 1; }
-    }
-    const int I2 = base2 + s * tq2;
-    float fr = (float)s * sf;
-    int I;
-    if (I2 & 1) { I = (I2 - 1) >> 1; fr += 0.5f; }
-    else { I = I2 >> 1; }
-    if (fr < 0.f) { fr += 1.f; I -= 1; }
-    else if (fr >= 1.f) { fr -= 1.f; I += 1; }
-    const int rows2 = 2 * p.n_theta;
-    I %= rows2;
-    if (I < 0) I += rows2;
-    c.t0 = I;
-    c.tf = fr;
-  }
-  return c;
+__global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab, int H, double dnu, double df,
+                                                        double tscale, int nearest) {
+  const long long count = (long long)(H + 1) * (H + 1);
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int a = (int)(i / (H + 1)), b = (int)(i % (H + 1));
+  const int L = 2 * H;
+  // numpy: fftfreq(L)[k] * L * dnu with index L/2 -> -L/2 (magnitude H)
+  const double nu1 = ((double)a * (1.0 / L)) * L * dnu;
+  const double nu2 = ((double)b * (1.0 / L)) * L * dnu;
+  const double ri = hypot(nu1, nu2) / df;
+  const double tq = atan2(nu2, nu1) * tscale;
+  const int top = H - 1;
+  double rfl = floor(ri);
+  int r0 = (int)rfl;
+  int qr = (int)rint((ri - rfl) * 65536.0);
+  if (qr >= 65536) { qr = 0; ++r0; }
+  double tfl = floor(tq);
+  int t0 = (int)tfl;
+  int qt = (int)rint((tq - tfl) * 65536.0);
+  if (qt >= 65536) { qt = 0; ++t0; }
+  const bool inside = nearest ? (rint(ri) <= (double)top) : (ri <= (double)top);
+  uint2 e;
+  e.x = (uint32_t)(inside ? (r0 & 0xFFFF) : 0xFFFF) | ((uint32_t)t0 << 16);
+  e.y = (uint32_t)qr | ((uint32_t)qt << 16);
+  tab[i] = e;
 }
 
-// polar sample P(t, r) of the full circle: mirror rows are conjugates for
-// half-turn input (fourier_bp.py:302-311; SURVEY.md finding 2)
+// polar sample P(t, r) of the full circle; rows t >= V of half-turn input are
+// the conjugate mirror (fourier_bp.py:302-311; SURVEY.md finding 2)
 __device__ __forceinline__ float2 polar_at(const DevPlan& p, const float2* __restrict__ pol, int t, int r) {
-  if (p.full_turn) return __ldg(pol + (size_t)t * p.H + r);
-  if (t < p.n_theta) return __ldg(pol + (size_t)t * p.H + r);
-  const float2 v = __ldg(pol + (size_t)(t - p.n_theta) * p.H + r);
-  return make_float2(v.x, -v.y);
+  const bool mirror = !p.full_turn && t >= p.n_theta;
+  const int row = mirror ? t - p.n_theta : t;
+  float2 v = __ldg(pol + (size_t)row * p.H + r);
+  if (mirror) v.y = -v.y;
+  return v;
 }
 
 // interpolated, modulated lattice value C(as, bs) (fourier_bp.py:389-407, 427-430)
-__device__ __forceinline__ float2 lattice_value(const DevPlan& p, const float2* __restrict__ pol,
-                                                const float2* __restrict__ com, int as, int bs) {
-  const NodeCoord c = node_coord(p, as, bs);
+__device__ __forceinline__ float2 lattice_value(const DevPlan& p, const uint2* __restrict__ tab,
+                                                const float2* __restrict__ pol, const float2* __restrict__ com,
+                                                int as, int bs) {
+  const int aa = as < 0 ? -as : as, ab = bs < 0 ? -bs : bs;
+  const uint2 e = __ldg(tab + (size_t)aa * (p.H + 1) + ab);
+  const int r0 = (int)(e.x & 0xFFFFu);
+  if (r0 == 0xFFFF) return make_float2(0.f, 0.f);
+  const int I = (int)(e.x >> 16);
+  const int qr = (int)(e.y & 0xFFFFu);
+  int qt = (int)(e.y >> 16);
+  // full angle from the first-quadrant angle tq = I + qt/65536
+  const int V = p.n_theta, rows2 = 2 * V;
+  int t0;
+  if ((as < 0) == (bs < 0)) {
+    t0 = as < 0 ? V + I : I;               // quadrants 1 and 3: base + tq
+  } else {
+    const int base = as < 0 ? V : rows2;   // quadrants 2 and 4: base - tq
+    if (qt == 0) t0 = base - I;
+    else { t0 = base - I - 1; qt = 65536 - qt; }
+  }
+  if (t0 >= rows2) t0 -= rows2;
   const int top = p.H - 1;
-  const int rows2 = 2 * p.n_theta;
   float2 val;
   if (p.interp == 0) {
-    if (c.r0 > top || (c.r0 == top && c.rf > 0.f)) return make_float2(0.f, 0.f);
-    const int ra = min(c.r0, top), rb = min(c.r0 + 1, top);
-    const int t1 = c.t0 + 1 == rows2 ? 0 : c.t0 + 1;
-    const float2 p00 = polar_at(p, pol, c.t0, ra), p01 = polar_at(p, pol, c.t0, rb);
+    const float rf = (float)qr * (1.f / 65536.f), tf = (float)qt * (1.f / 65536.f);
+    const int ra = r0, rb = min(r0 + 1, top);
+    const int t1 = t0 + 1 == rows2 ? 0 : t0 + 1;
+    const float2 p00 = polar_at(p, pol, t0, ra), p01 = polar_at(p, pol, t0, rb);
     const float2 p10 = polar_at(p, pol, t1, ra), p11 = polar_at(p, pol, t1, rb);
     const float2 c0 = __ldg(com + ra), c1 = __ldg(com + rb);
-    const float rf = c.rf, tf = c.tf;
     const float2 r0v = make_float2(fmaf(rf, p01.x - p00.x, p00.x), fmaf(rf, p01.y - p00.y, p00.y));
     const float2 r1v = make_float2(fmaf(rf, p11.x - p10.x, p10.x), fmaf(rf, p11.y - p10.y, p10.y));
     const float2 cv = make_float2(fmaf(rf, c1.x - c0.x, c0.x), fmaf(rf, c1.y - c0.y, c0.y));
     val = make_float2(fmaf(tf, r1v.x - r0v.x, r0v.x) + cv.x, fmaf(tf, r1v.y - r0v.y, r0v.y) + cv.y);
   } else {
-    // nearest: np.rint (half to even) on both coordinates (fourier_bp.py:234-238)
-    int ir = c.r0 + ((c.rf > 0.5f || (c.rf == 0.5f && (c.r0 & 1))) ? 1 : 0);
-    if (ir > top) return make_float2(0.f, 0.f);
-    int it = c.t0 + ((c.tf > 0.5f || (c.tf == 0.5f && (c.t0 & 1))) ? 1 : 0);
+    // np.rint (half to even) on both coordinates (fourier_bp.py:234-238)
+    const int ir = r0 + ((qr > 32768 || (qr == 32768 && (r0 & 1))) ? 1 : 0);
+    int it = t0 + ((qt > 32768 || (qt == 32768 && (t0 & 1))) ? 1 : 0);
     if (it >= rows2) it -= rows2;
     const float2 pv = polar_at(p, pol, it, ir);
     const float2 cv = __ldg(com + ir);
@@ -429,10 +405,17 @@ __device__ __forceinline__ float2 lattice_value(const DevPlan& p, const float2* 
   return val;
 }
 
+// K2 -> K3 intermediate: [B][ceil(n/4)][H+1][4] complex (4-row tiles = one
+// 32-byte sector per (tile, column)), so K2's column stores and K3's row-pair
+// loads both move whole sectors.
+__device__ __forceinline__ size_t col_index(int H, int m2, int a) {
+  return ((size_t)(m2 >> 2) * (H + 1) + a) * 4 + (m2 & 3);
+}
+
 // ---------------------------------------------------------------------------
 // K2: gather + IFFT along k2 for one Cartesian column a in [0, H]
 // ---------------------------------------------------------------------------
-template <int L>
+template <int L, bool CROP_HALF>
 __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work w) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
@@ -445,6 +428,7 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
   const int as = a < H ? a : -H;
   const float2* pol = w.polar + (size_t)q * p.rows * H;
   const float2* com = w.common + (size_t)q * H;
+  const uint2* tab = p.gridtab;
   float2 v[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
@@ -452,12 +436,12 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
     if (active) {
       const int b = t + i * TPF;
       const int bs = b < H ? b : b - L;
-      val = lattice_value(p, pol, com, as, bs);
+      val = lattice_value(p, tab, pol, com, as, bs);
       // Hermitian part: 0.5 (C[k] + conj C[-k mod L]) (.real of ifft2, fourier_bp.py:431)
       if (p.full_turn || (p.nyq && (a == H || b == H))) {
         const int pa = as == -H ? -H : -as;
         const int pb = bs == -H ? -H : -bs;
-        const float2 m = lattice_value(p, pol, com, pa, pb);
+        const float2 m = lattice_value(p, tab, pol, com, pa, pb);
         val = make_float2(0.5f * (val.x + m.x), 0.5f * (val.y - m.y));
       }
     }
@@ -465,18 +449,20 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
   }
   fft<L, true>(v, smem, t, active, p.tw_L);
   if (active) {
-    float2* out = w.columns + ((size_t)q * (H + 1) + a) * p.n;
+    float2* out = w.columns + (size_t)q * p.col_slice;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const int idx = t + i * TPF;
       const int m2 = (idx + p.n_half) & (L - 1);
-      if (m2 < p.n) out[m2] = v[i];
+      // n = L/2: the kept rows are i < RPT/4 or i >= 3 RPT/4 (others DCE'd)
+      const bool keep = CROP_HALF ? (i < RPT / 4 || i >= 3 * RPT / 4) : (m2 < p.n);
+      if (keep) out[col_index(H, m2, a)] = v[i];
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// K3: C2R along k1 for a pair of output rows + epilogue
+// K3: C2R along k1 for a tile of 4 output rows (two packed pairs) + epilogue
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float coverage(float x1, float x2) {
   // fourier_bp.py:204-220 : pi inside the unit circle, 2 asin(1/r) outside
@@ -484,7 +470,7 @@ __device__ __forceinline__ float coverage(float x1, float x2) {
   return r > 1.f ? 2.f * asinf(1.f / r) : 3.14159265358979323846f;
 }
 
-template <int L>
+template <int L, bool CROP_HALF>
 __global__ void __launch_bounds__(KShape<L>::THREADS) k3_rows(DevPlan p, Work w, float* __restrict__ img,
                                                               float out_scale) {
   using K = KShape<L>;
@@ -493,52 +479,58 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k3_rows(DevPlan p, Work w,
   extern __shared__ float2 smem[];
   const int t = threadIdx.x;
   const bool active = t < TPF;
-  const int m2a = 2 * blockIdx.x, m2b = m2a + 1;
+  const int tile = blockIdx.x;
   const int q = blockIdx.y;
   const int n = p.n;
-  const bool hasb = m2b < n;
-  const float2* G = w.columns + (size_t)q * (H + 1) * n;
-  float2 v[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    float2 z = make_float2(0.f, 0.f);
-    if (active) {
-      const int a = t + i * TPF;
-      const int ar = a <= H ? a : L - a;
-      const float2* row = G + (size_t)ar * n;
-      float2 ga = __ldg(row + m2a);
-      float2 gb = hasb ? __ldg(row + m2b) : make_float2(0.f, 0.f);
-      if (a == 0 || a == H) { ga.y = 0.f; gb.y = 0.f; }
-      if (a > H) { ga.y = -ga.y; gb.y = -gb.y; }
-      z = make_float2(ga.x - gb.y, ga.y + gb.x);  // ga + i gb
-    }
-    v[i] = z;
-  }
-  fft<L, true>(v, smem, t, active, p.tw_L);
+  const float2* G = w.columns + (size_t)q * p.col_slice + (size_t)tile * (H + 1) * 4;
+  const float cm = w.coefmean[q];
+  const float inv_n = 2.f / (float)n;
   bool bad = false;
-  if (active) {
-    const float cm = w.coefmean[q];
-    const float inv_n = 2.f / (float)n;
-    const float x2a = -1.f + ((float)m2a + 0.5f) * inv_n;
-    const float x2b = -1.f + ((float)m2b + 0.5f) * inv_n;
-    float* oa = img + ((size_t)q * n + m2a) * n;
-    float* ob = oa + n;
+  for (int pair = 0; pair < 2; ++pair) {
+    const int m2a = 4 * tile + 2 * pair, m2b = m2a + 1;
+    if (m2a >= n) break;  // uniform across the CTA
+    const bool hasb = m2b < n;
+    float2 v[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
-      const int idx = t + i * TPF;
-      const int m1 = (idx + p.n_half) & (L - 1);
-      if (m1 < n) {
-        const float x1 = -1.f + ((float)m1 + 0.5f) * inv_n;
-        const float ra = fmaf(v[i].x, p.img_scale, cm * coverage(x1, x2a)) * out_scale;
-        oa[m1] = ra;
-        bad |= !isfinite(ra);
-        if (hasb) {
-          const float rb = fmaf(v[i].y, p.img_scale, cm * coverage(x1, x2b)) * out_scale;
-          ob[m1] = rb;
-          bad |= !isfinite(rb);
+      float2 z = make_float2(0.f, 0.f);
+      if (active) {
+        const int a = t + i * TPF;
+        const int ar = a <= H ? a : L - a;
+        const float4 g = __ldg(reinterpret_cast<const float4*>(G + (size_t)ar * 4 + 2 * pair));
+        float2 ga = make_float2(g.x, g.y);
+        float2 gb = hasb ? make_float2(g.z, g.w) : make_float2(0.f, 0.f);
+        if (a == 0 || a == H) { ga.y = 0.f; gb.y = 0.f; }
+        if (a > H) { ga.y = -ga.y; gb.y = -gb.y; }
+        z = make_float2(ga.x - gb.y, ga.y + gb.x);  // ga + i gb
+      }
+      v[i] = z;
+    }
+    fft<L, true>(v, smem, t, active, p.tw_L);
+    if (active) {
+      const float x2a = -1.f + ((float)m2a + 0.5f) * inv_n;
+      const float x2b = -1.f + ((float)m2b + 0.5f) * inv_n;
+      float* oa = img + ((size_t)q * n + m2a) * n;
+      float* ob = oa + n;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int idx = t + i * TPF;
+        const int m1 = (idx + p.n_half) & (L - 1);
+        const bool keep = CROP_HALF ? (i < RPT / 4 || i >= 3 * RPT / 4) : (m1 < n);
+        if (keep) {
+          const float x1 = -1.f + ((float)m1 + 0.5f) * inv_n;
+          const float ra = fmaf(v[i].x, p.img_scale, cm * coverage(x1, x2a)) * out_scale;
+          oa[m1] = ra;
+          bad |= !isfinite(ra);
+          if (hasb) {
+            const float rb = fmaf(v[i].y, p.img_scale, cm * coverage(x1, x2b)) * out_scale;
+            ob[m1] = rb;
+            bad |= !isfinite(rb);
+          }
         }
       }
     }
+    __syncthreads();  // smem reuse by the next pair
   }
   if (bad) atomicOr(&w.status[1], 1);
 }

@@ -118,7 +118,9 @@ def test_each_kernel_against_three_kernel_oracle(name):
     assert np.linalg.norm(com - Chat) <= 2e-5 * np.linalg.norm(Chat) + 1e-6 * np.linalg.norm(Ahat) / np.sqrt(rows)
     cm = view(lay["coefmean"], 1, torch.float32)[0]
     assert abs(cm - coef_mean) <= 1e-5 * max(1.0, abs(coef_mean))
-    cols = view(lay["columns"], (H + 1) * n * 2, torch.float32).view(np.complex64).reshape(H + 1, n)
+    tiles = (n + 3) // 4  # K2 output is stored in 4-row tiles [tile][a][4]
+    cols = view(lay["columns"], tiles * (H + 1) * 4 * 2, torch.float32).view(np.complex64)
+    cols = cols.reshape(tiles, H + 1, 4).transpose(1, 0, 2).reshape(H + 1, tiles * 4)[:, :n]
     assert rel_l2(cols, G) < 5e-5
 
 
