@@ -124,7 +124,10 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
 template <int L>
 struct Launch {
   using K = tb::KShape<L>;
-  static size_t smem_k1(const tb_plan* p) { return K::BUF * sizeof(float2) + (size_t)std::max(p->S, 1) * 4; }
+  static size_t smem_k1(const tb_plan* p) {
+    // FFT buffer + support sums + two TMA staging slots of a row pair + 2 mbarriers
+    return K::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 + (size_t)4 * p->n_t * 4 + 16;
+  }
   static size_t smem_k1b(const tb_plan* p) {
     return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::K1B_THREADS * 4;
   }

@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const
   extern __shared__ float2 smem[];
   float2* buf = smem;
   float* sacc = reinterpret_cast<float*>(smem + K::BUF);
+  // two staging slots for the next row pair (TMA bulk copies), 16-B aligned
+  float* stage = sacc + ((p.S + 3) & ~3);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + 4 * p.n_t);
   const int t = threadIdx.x;
   const bool active = t < TPF;
   const int q = blockIdx.y;
@@ -91,29 +94,68 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const
   const int pr_begin = g * w.pairs_per_cta;
   const int pr_end = min(npairs, pr_begin + w.pairs_per_cta);
   const int H = L / 2;
+  const float* slice = sino + (size_t)q * p.rows * p.n_t;
+  // bulk copies need 16-byte aligned rows; otherwise read rows directly
+  const bool bulk = (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0);
+  auto issue = [&](int pr, int slot) {
+    const int j0 = 2 * pr;
+    const int nrow = (2 * pr + 1 < p.rows) ? 2 : 1;
+    const uint32_t bytes = (uint32_t)(nrow * p.n_t * 4);
+    mbar_expect_tx(&bars[slot], bytes);
+    bulk_g2s(stage + slot * 2 * p.n_t, slice + (size_t)j0 * p.n_t, bytes, &bars[slot]);
+  };
 
   for (int i = t; i < p.S; i += blockDim.x) sacc[i] = 0.f;
+  if (bulk && t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
   __syncthreads();
+  if (bulk && t == 0 && pr_begin < pr_end) issue(pr_begin, 0);
   bool bad = false;
+  uint32_t phase[2] = {0u, 0u};
 
   for (int pr = pr_begin; pr < pr_end; ++pr) {
     const int j0 = 2 * pr, j1 = 2 * pr + 1;
     const bool has1 = j1 < p.rows;
-    const float* y0 = sino + ((size_t)q * p.rows + j0) * p.n_t;
-    const float* y1 = y0 + p.n_t;
+    const int slot = (pr - pr_begin) & 1;
     float2 v[RPT];
+    if (bulk) {
+      // prefetch the next pair into the other slot (freed by the barrier that
+      // closed the previous iteration), then wait for this pair's rows
+      if (t == 0 && pr + 1 < pr_end) issue(pr + 1, slot ^ 1);
+      mbar_wait(&bars[slot], phase[slot]);
+      phase[slot] ^= 1u;
+      const float* r0 = stage + slot * 2 * p.n_t;
+      const float* r1 = r0 + p.n_t;
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int idx = t + i * TPF;
-      float a = 0.f, b = 0.f;
-      // n_t <= L/2 always (L >= pad_factor * n_t, pad_factor >= 2): the upper
-      // half of every padded row is a compile-time zero (pruned first pass)
-      if (i < RPT / 2 && active && idx < p.n_t) {
-        a = __ldg(y0 + idx);
-        if (has1) b = __ldg(y1 + idx);
-        bad |= !isfinite(a) || !isfinite(b);
+      for (int i = 0; i < RPT; ++i) {
+        const int idx = t + i * TPF;
+        float a = 0.f, b = 0.f;
+        if (i < RPT / 2 && active && idx < p.n_t) {
+          a = r0[idx];
+          if (has1) b = r1[idx];
+          bad |= !isfinite(a) || !isfinite(b);
+        }
+        v[i] = make_float2(a, b);
       }
-      v[i] = make_float2(a, b);
+    } else {
+      const float* y0 = slice + (size_t)j0 * p.n_t;
+      const float* y1 = y0 + p.n_t;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int idx = t + i * TPF;
+        float a = 0.f, b = 0.f;
+        // n_t <= L/2 always (L >= pad_factor * n_t, pad_factor >= 2): the upper
+        // half of every padded row is a compile-time zero (pruned first pass)
+        if (i < RPT / 2 && active && idx < p.n_t) {
+          a = __ldg(y0 + idx);
+          if (has1) b = __ldg(y1 + idx);
+          bad |= !isfinite(a) || !isfinite(b);
+        }
+        v[i] = make_float2(a, b);
+      }
     }
     if constexpr (RAMP) {
       fft<L, false>(v, buf, t, active, p.tw_np);
@@ -405,6 +447,39 @@ __device__ __forceinline__ float2 lattice_value(const DevPlan& p, const uint2* _
   return val;
 }
 
+// Decoded gridding node: polar corners (t0|t1, ra|rb) and bilinear weights.
+struct GridNode {
+  int t0, t1, ra, rb;
+  float rf, tf;
+  bool inside;
+};
+
+// full-angle node from a first-quadrant table entry (see build_grid_table)
+__device__ __forceinline__ GridNode decode_node(const DevPlan& p, uint2 e, int as, int bs) {
+  GridNode g;
+  const int r0 = (int)(e.x & 0xFFFFu);
+  g.inside = r0 != 0xFFFF;
+  const int I = (int)(e.x >> 16);
+  int qt = (int)(e.y >> 16);
+  const int V = p.n_theta, rows2 = 2 * V;
+  int t0;
+  if ((as < 0) == (bs < 0)) {
+    t0 = as < 0 ? V + I : I;
+  } else {
+    const int base = as < 0 ? V : rows2;
+    if (qt == 0) t0 = base - I;
+    else { t0 = base - I - 1; qt = 65536 - qt; }
+  }
+  if (t0 >= rows2) t0 -= rows2;
+  g.t0 = t0;
+  g.t1 = t0 + 1 == rows2 ? 0 : t0 + 1;
+  g.ra = g.inside ? r0 : 0;
+  g.rb = g.inside ? min(r0 + 1, p.H - 1) : 0;
+  g.rf = (float)(e.y & 0xFFFFu) * (1.f / 65536.f);
+  g.tf = (float)qt * (1.f / 65536.f);
+  return g;
+}
+
 // K2 -> K3 intermediate: [B][ceil(n/4)][H+1][4] complex (4-row tiles = one
 // 32-byte sector per (tile, column)), so K2's column stores and K3's row-pair
 // loads both move whole sectors.
@@ -430,22 +505,78 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
   const float2* com = w.common + (size_t)q * H;
   const uint2* tab = p.gridtab;
   float2 v[RPT];
+  if (p.interp == 0 && !p.full_turn) {
+    // bilinear fast path, software-pipelined: all table entries first, then
+    // the corner gathers of NB nodes at a time (keeps ~7*NB loads in flight)
+    uint2 e[RPT];
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    float2 val = make_float2(0.f, 0.f);
-    if (active) {
+    for (int i = 0; i < RPT; ++i) {
       const int b = t + i * TPF;
-      const int bs = b < H ? b : b - L;
-      val = lattice_value(p, tab, pol, com, as, bs);
-      // Hermitian part: 0.5 (C[k] + conj C[-k mod L]) (.real of ifft2, fourier_bp.py:431)
-      if (p.full_turn || (p.nyq && (a == H || b == H))) {
-        const int pa = as == -H ? -H : -as;
-        const int pb = bs == -H ? -H : -bs;
-        const float2 m = lattice_value(p, tab, pol, com, pa, pb);
-        val = make_float2(0.5f * (val.x + m.x), 0.5f * (val.y - m.y));
+      const int ab = b <= H ? b : L - b;
+      e[i] = active ? __ldg(tab + (size_t)a * (H + 1) + ab) : make_uint2(0xFFFFu, 0u);
+    }
+    const float2 ma = p.has_mod ? __ldg(p.modt + (as & (L - 1))) : make_float2(1.f, 0.f);
+    constexpr int NB = 2;
+#pragma unroll
+    for (int c = 0; c < RPT; c += NB) {
+      GridNode g[NB];
+      float2 p00[NB], p01[NB], p10[NB], p11[NB], c0[NB], c1[NB], mb[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int b = t + (c + j) * TPF;
+        const int bs = b < H ? b : b - L;
+        g[j] = decode_node(p, e[c + j], as, bs);
+        p00[j] = polar_at(p, pol, g[j].t0, g[j].ra);
+        p01[j] = polar_at(p, pol, g[j].t0, g[j].rb);
+        p10[j] = polar_at(p, pol, g[j].t1, g[j].ra);
+        p11[j] = polar_at(p, pol, g[j].t1, g[j].rb);
+        c0[j] = __ldg(com + g[j].ra);
+        c1[j] = __ldg(com + g[j].rb);
+        mb[j] = p.has_mod ? __ldg(p.modt + (bs & (L - 1))) : make_float2(1.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const float rf = g[j].rf, tf = g[j].tf;
+        const float2 r0v = make_float2(fmaf(rf, p01[j].x - p00[j].x, p00[j].x), fmaf(rf, p01[j].y - p00[j].y, p00[j].y));
+        const float2 r1v = make_float2(fmaf(rf, p11[j].x - p10[j].x, p10[j].x), fmaf(rf, p11[j].y - p10[j].y, p10[j].y));
+        const float2 cv = make_float2(fmaf(rf, c1[j].x - c0[j].x, c0[j].x), fmaf(rf, c1[j].y - c0[j].y, c0[j].y));
+        float2 val = make_float2(fmaf(tf, r1v.x - r0v.x, r0v.x) + cv.x, fmaf(tf, r1v.y - r0v.y, r0v.y) + cv.y);
+        if (p.has_mod) val = cmul(val, cmul(ma, mb[j]));
+        v[c + j] = g[j].inside ? val : make_float2(0.f, 0.f);
       }
     }
-    v[i] = val;
+    if (p.nyq && active) {
+      // Nyquist lines: Hermitian part 0.5 (C[k] + conj C[-k mod L]) (.real of ifft2, fourier_bp.py:431)
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int b = t + i * TPF;
+        if (a == H || b == H) {
+          const int bs = b < H ? b : b - L;
+          const int pa = as == -H ? -H : -as;
+          const int pb = bs == -H ? -H : -bs;
+          const float2 m = lattice_value(p, tab, pol, com, pa, pb);
+          v[i] = make_float2(0.5f * (v[i].x + m.x), 0.5f * (v[i].y - m.y));
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      float2 val = make_float2(0.f, 0.f);
+      if (active) {
+        const int b = t + i * TPF;
+        const int bs = b < H ? b : b - L;
+        val = lattice_value(p, tab, pol, com, as, bs);
+        // Hermitian part: 0.5 (C[k] + conj C[-k mod L]) (.real of ifft2, fourier_bp.py:431)
+        if (p.full_turn || (p.nyq && (a == H || b == H))) {
+          const int pa = as == -H ? -H : -as;
+          const int pb = bs == -H ? -H : -bs;
+          const float2 m = lattice_value(p, tab, pol, com, pa, pb);
+          val = make_float2(0.5f * (val.x + m.x), 0.5f * (val.y - m.y));
+        }
+      }
+      v[i] = val;
+    }
   }
   fft<L, true>(v, smem, t, active, p.tw_L);
   if (active) {
