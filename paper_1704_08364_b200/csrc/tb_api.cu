@@ -76,7 +76,7 @@ namespace {
 constexpr int kLanes = 2;  // concurrent launch groups (streams) per call
 
 struct Layout {
-  size_t polar, rowcoef, part, common, coefmean, columns, filtered, status, total;
+  size_t polar, rowcoef, part, common, common2, coefmean, columns, filtered, status, total;
   size_t lane_bytes;  // stride between the per-lane regions (all but status)
 };
 
@@ -89,10 +89,11 @@ Layout layout_for(const tb_plan* p, int B) {
     return o;
   };
   l.status = take(2 * sizeof(int));  // first: its offset does not depend on the batch
-  l.polar = take((size_t)B * p->rows * p->H * sizeof(float2));
+  l.polar = take((size_t)B * p->dp.prow * p->H * sizeof(float2));
   l.rowcoef = take((size_t)B * p->rows * sizeof(float));
   l.part = take((size_t)B * p->groups * std::max(p->S, 1) * sizeof(float));
   l.common = take((size_t)B * p->H * sizeof(float2));
+  l.common2 = take((size_t)B * p->H * sizeof(float2));
   l.coefmean = take((size_t)B * sizeof(float));
   l.columns = take((size_t)B * p->dp.col_slice * sizeof(float2));
   l.filtered = take((size_t)B * p->rows * p->n_t * sizeof(float));
@@ -109,6 +110,7 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   w.rowcoef = reinterpret_cast<float*>(base + l.rowcoef);
   w.part = reinterpret_cast<float*>(base + l.part);
   w.common = reinterpret_cast<float2*>(base + l.common);
+  w.common2 = reinterpret_cast<float2*>(base + l.common2);
   w.coefmean = reinterpret_cast<float*>(base + l.coefmean);
   w.columns = reinterpret_cast<float2*>(base + l.columns);
   w.filtered = reinterpret_cast<float*>(base + l.filtered);
@@ -129,7 +131,8 @@ struct Launch {
     return K::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 + (size_t)4 * p->n_t * 4 + 16;
   }
   static size_t smem_k1b(const tb_plan* p) {
-    return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::K1B_THREADS * 4;
+    return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::K1B_THREADS * 4 +
+           (size_t)(L / 2) * 4;
   }
   static size_t smem_fft() { return K::BUF * sizeof(float2); }
 
@@ -587,6 +590,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   dp.rho = reinterpret_cast<const float2*>(b + o_rho);
   dp.modt = reinterpret_cast<const float2*>(b + o_mod);
   dp.col_slice = (size_t)((n + 3) / 4) * (H + 1) * 4;
+  dp.prow = d->full_turn ? 2 * V : V + 1;
   dp.ss_cs = reinterpret_cast<const double2*>(b + o_ss);
 
   // gridding table (fourier_bp.py:222-249), built on the device in fp64

@@ -46,6 +46,7 @@ struct DevPlan {
   const float2* modt;   // [L]    half-node modulation (or null)
   const double2* ss_cs; // [A]    (cos, sin) of the input angles
   const uint2* gridtab; // [(H+1)^2] first-quadrant gridding table
+  int prow;             // polar rows per slice: V + 1 (half turn, row V = conj row 0) or 2V
   size_t col_slice;     // complex elements per slice of the K2 output (tiled)
 };
 
@@ -54,6 +55,7 @@ struct Work {
   float* rowcoef;
   float* part;
   float2* common;
+  float2* common2;  // [B][H] (Re C[r], Re C[min(r+1, H-1)]) for the half-turn fast path
   float* coefmean;
   float2* columns;
   float* filtered;
@@ -195,8 +197,10 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const
     __syncthreads();
     const float2 z0 = buf[0];
     const float a0 = z0.x * p.inv_nt, a1 = z0.y * p.inv_nt;
-    float2* out0 = w.polar + ((size_t)q * p.rows + j0) * H;
+    float2* out0 = w.polar + ((size_t)q * p.prow + j0) * H;
     float2* out1 = out0 + H;
+    // half turn: row V holds conj(row 0), the angle-pi mirror (fourier_bp.py:310)
+    float2* outm = (!p.full_turn && j0 == 0) ? w.polar + ((size_t)q * p.prow + p.n_theta) * H : nullptr;
     if (active) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
@@ -214,6 +218,7 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const
           if (k == 0) { A0 = make_float2(0.f, 0.f); A1 = A0; }
           out0[k] = A0;
           if (has1) out1[k] = A1;
+          if (outm) outm[k] = make_float2(A0.x, -A0.y);
         }
       }
     }
@@ -290,7 +295,8 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
   float2* buf = smem;
   float* cs = reinterpret_cast<float*>(smem + K::BUF);
   float* bm = cs + p.S;
-  float* red = bm + p.S;  // [blockDim]
+  float* red = bm + p.S;  // [2 * blockDim]
+  float* buf2 = red + 2 * blockDim.x;  // [H] real part of the common row
   const int t = threadIdx.x;
   const bool active = t < TPF;
   const int q = blockIdx.x;
@@ -342,11 +348,17 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
         float2 C = cmul(ps, v[i]);
         C = make_float2(fmaf(-c, rh.x, C.x), fmaf(-c, rh.y, C.y));
         if (k == 0) C = make_float2(0.f, 0.f);
+        // half turn: the windowed mean row is symmetric in t, so C is real
+        if (!p.full_turn) C.y = 0.f;
         out[k] = C;
+        buf2[k] = C.x;
       }
     }
   }
   if (t == 0) w.coefmean[q] = amean + c;
+  __syncthreads();
+  float2* out2 = w.common2 + (size_t)q * H;
+  for (int k = t; k < H; k += blockDim.x) out2[k] = make_float2(buf2[k], buf2[min(k + 1, H - 1)]);
 }
 
 // ---------------------------------------------------------------------------
@@ -501,13 +513,17 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
   const int a = blockIdx.x;
   const int q = blockIdx.y;
   const int as = a < H ? a : -H;
-  const float2* pol = w.polar + (size_t)q * p.rows * H;
+  const float2* pol = w.polar + (size_t)q * p.prow * H;
   const float2* com = w.common + (size_t)q * H;
   const uint2* tab = p.gridtab;
   float2 v[RPT];
   if (p.interp == 0 && !p.full_turn) {
-    // bilinear fast path, software-pipelined: all table entries first, then
-    // the corner gathers of NB nodes at a time (keeps ~7*NB loads in flight)
+    // Half-turn bilinear fast path.  A node in the lower half plane (b < 0)
+    // is the conjugate of its point reflection (-a, -b), which lies in the
+    // upper half plane and reads polar rows t in [0, V] (row V = conj row 0):
+    // no per-corner mirror logic.  Software-pipelined: all table entries
+    // first, then the corner gathers of NB nodes at a time.
+    const float2* com2 = w.common2 + (size_t)q * H;
     uint2 e[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -515,38 +531,57 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
       const int ab = b <= H ? b : L - b;
       e[i] = active ? __ldg(tab + (size_t)a * (H + 1) + ab) : make_uint2(0xFFFFu, 0u);
     }
-    const float2 ma = p.has_mod ? __ldg(p.modt + (as & (L - 1))) : make_float2(1.f, 0.f);
-    constexpr int NB = 2;
+    const int V = p.n_theta;
+    constexpr int NB = 4;
 #pragma unroll
     for (int c = 0; c < RPT; c += NB) {
-      GridNode g[NB];
-      float2 p00[NB], p01[NB], p10[NB], p11[NB], c0[NB], c1[NB], mb[NB];
+      float2 p00[NB], p01[NB], p10[NB], p11[NB], cc[NB], mb[NB];
+      float rf[NB], tf[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const int b = t + (c + j) * TPF;
         const int bs = b < H ? b : b - L;
-        g[j] = decode_node(p, e[c + j], as, bs);
-        p00[j] = polar_at(p, pol, g[j].t0, g[j].ra);
-        p01[j] = polar_at(p, pol, g[j].t0, g[j].rb);
-        p10[j] = polar_at(p, pol, g[j].t1, g[j].ra);
-        p11[j] = polar_at(p, pol, g[j].t1, g[j].rb);
-        c0[j] = __ldg(com + g[j].ra);
-        c1[j] = __ldg(com + g[j].rb);
+        const uint2 ej = e[c + j];
+        const int r0 = (int)(ej.x & 0xFFFFu);
+        const int ra = r0 == 0xFFFF ? 0 : r0;
+        const int rb = min(ra + 1, H - 1);
+        const int I = (int)(ej.x >> 16);
+        int qt = (int)(ej.y >> 16);
+        const bool flip = (as < 0) != (bs < 0);  // effective a < 0 after reflection
+        int t0 = I;
+        if (flip) {
+          t0 = qt ? V - I - 1 : V - I;
+          qt = qt ? 65536 - qt : 0;
+        }
+        const float2* row0 = pol + (size_t)t0 * H;
+        p00[j] = __ldg(row0 + ra);
+        p01[j] = __ldg(row0 + rb);
+        p10[j] = __ldg(row0 + H + ra);
+        p11[j] = __ldg(row0 + H + rb);
+        cc[j] = __ldg(com2 + ra);
         mb[j] = p.has_mod ? __ldg(p.modt + (bs & (L - 1))) : make_float2(1.f, 0.f);
+        rf[j] = (float)(ej.y & 0xFFFFu) * (1.f / 65536.f);
+        tf[j] = (float)qt * (1.f / 65536.f);
       }
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const float rf = g[j].rf, tf = g[j].tf;
-        const float2 r0v = make_float2(fmaf(rf, p01[j].x - p00[j].x, p00[j].x), fmaf(rf, p01[j].y - p00[j].y, p00[j].y));
-        const float2 r1v = make_float2(fmaf(rf, p11[j].x - p10[j].x, p10[j].x), fmaf(rf, p11[j].y - p10[j].y, p10[j].y));
-        const float2 cv = make_float2(fmaf(rf, c1[j].x - c0[j].x, c0[j].x), fmaf(rf, c1[j].y - c0[j].y, c0[j].y));
-        float2 val = make_float2(fmaf(tf, r1v.x - r0v.x, r0v.x) + cv.x, fmaf(tf, r1v.y - r0v.y, r0v.y) + cv.y);
-        if (p.has_mod) val = cmul(val, cmul(ma, mb[j]));
-        v[c + j] = g[j].inside ? val : make_float2(0.f, 0.f);
+        const int b = t + (c + j) * TPF;
+        const bool lower = b >= H;  // bs < 0 (index H is -L/2)
+        const float r = rf[j], u = tf[j];
+        const float2 r0v = make_float2(fmaf(r, p01[j].x - p00[j].x, p00[j].x), fmaf(r, p01[j].y - p00[j].y, p00[j].y));
+        const float2 r1v = make_float2(fmaf(r, p11[j].x - p10[j].x, p10[j].x), fmaf(r, p11[j].y - p10[j].y, p10[j].y));
+        float2 val = make_float2(fmaf(u, r1v.x - r0v.x, r0v.x) + fmaf(r, cc[j].y - cc[j].x, cc[j].x),
+                                 fmaf(u, r1v.y - r0v.y, r0v.y));
+        if (lower) val.y = -val.y;
+        if (p.has_mod) val = cmul(val, mb[j]);
+        v[c + j] = ((e[c + j].x & 0xFFFFu) == 0xFFFFu) ? make_float2(0.f, 0.f) : val;
       }
     }
     if (p.nyq && active) {
-      // Nyquist lines: Hermitian part 0.5 (C[k] + conj C[-k mod L]) (.real of ifft2, fourier_bp.py:431)
+      // Nyquist lines: Hermitian part 0.5 (C[k] + conj C[-k mod L]) of the fully
+      // modulated lattice (.real of ifft2, fourier_bp.py:431); the column
+      // factor M[a] is re-applied in K3, so divide it out here
+      const float2 ma = p.has_mod ? __ldg(p.modt + (as & (L - 1))) : make_float2(1.f, 0.f);
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const int b = t + i * TPF;
@@ -554,8 +589,10 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
           const int bs = b < H ? b : b - L;
           const int pa = as == -H ? -H : -as;
           const int pb = bs == -H ? -H : -bs;
+          const float2 c0 = lattice_value(p, tab, pol, com, as, bs);
           const float2 m = lattice_value(p, tab, pol, com, pa, pb);
-          v[i] = make_float2(0.5f * (v[i].x + m.x), 0.5f * (v[i].y - m.y));
+          const float2 hv = make_float2(0.5f * (c0.x + m.x), 0.5f * (c0.y - m.y));
+          v[i] = cmul(hv, make_float2(ma.x, -ma.y));
         }
       }
     }
@@ -573,6 +610,10 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
           const int pb = bs == -H ? -H : -bs;
           const float2 m = lattice_value(p, tab, pol, com, pa, pb);
           val = make_float2(0.5f * (val.x + m.x), 0.5f * (val.y - m.y));
+        }
+        if (p.has_mod) {  // K3 applies the column factor M[a]
+          const float2 ma = __ldg(p.modt + (as & (L - 1)));
+          val = cmul(val, make_float2(ma.x, -ma.y));
         }
       }
       v[i] = val;
@@ -631,6 +672,11 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k3_rows(DevPlan p, Work w,
         const float4 g = __ldg(reinterpret_cast<const float4*>(G + (size_t)ar * 4 + 2 * pair));
         float2 ga = make_float2(g.x, g.y);
         float2 gb = hasb ? make_float2(g.z, g.w) : make_float2(0.f, 0.f);
+        if (p.has_mod) {  // column half-node factor M[a] (fourier_bp.py:430)
+          const float2 ma = __ldg(p.modt + ar);
+          ga = cmul(ga, ma);
+          gb = cmul(gb, ma);
+        }
         if (a == 0 || a == H) { ga.y = 0.f; gb.y = 0.f; }
         if (a > H) { ga.y = -ga.y; gb.y = -gb.y; }
         z = make_float2(ga.x - gb.y, ga.y + gb.x);  // ga + i gb
