@@ -14,7 +14,7 @@ import re
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtb_bst.so")
+LIB_PATH = os.environ.get("TB_LIB_PATH") or os.path.join(HERE, "lib", "libtb_bst.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "tb_bst.h")
 
 TB_OK = 0

@@ -218,12 +218,25 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
     if constexpr (NS > 1) {
       float2 w = active ? __ldg(&tw[k * (N / (NS * R))]) : make_float2(1.f, 0.f);
       if (INV) w.y = -w.y;
-      float2 wp[R];
-      wp[1] = w;
+      // powers w^m, m < R, from w, w^2, w^3 and w^{4k} (<= 3 roundings each,
+      // ~10 live registers instead of R)
+      const float2 w2 = cmul(w, w);
+      const float2 w3 = cmul(w2, w);
+      x[b][1] = cmul(x[b][1], w);
+      if constexpr (R > 2) x[b][2] = cmul(x[b][2], w2);
+      if constexpr (R > 3) x[b][3] = cmul(x[b][3], w3);
+      if constexpr (R > 4) {
+        float2 w4k = cmul(w2, w2);
 #pragma unroll
-      for (int m = 2; m < R; ++m) wp[m] = (m & 1) ? cmul(wp[m - 1], wp[1]) : cmul(wp[m / 2], wp[m / 2]);
-#pragma unroll
-      for (int m = 1; m < R; ++m) x[b][m] = cmul(x[b][m], wp[m]);
+        for (int k = 4; k < R; k += 4) {
+          if (k == 8) w4k = cmul(w4k, w4k);
+          if (k == 12) w4k = cmul(w4k, cmul(w2, w2));
+          x[b][k] = cmul(x[b][k], w4k);
+          x[b][k + 1] = cmul(x[b][k + 1], cmul(w4k, w));
+          x[b][k + 2] = cmul(x[b][k + 2], cmul(w4k, w2));
+          x[b][k + 3] = cmul(x[b][k + 3], cmul(w4k, w3));
+        }
+      }
     }
     Dft<R, INV>::run(x[b]);
     if constexpr (LAST) {

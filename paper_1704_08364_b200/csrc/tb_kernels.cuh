@@ -73,13 +73,18 @@ struct KShape {
   // smem buffer (float2) for the FFT passes and the K1 Z_k / Z_{L-k} exchange
   static constexpr int BUF = S::SMEM > 0 ? S::SMEM : L;
   static constexpr int K1B_THREADS = THREADS < 512 ? 512 : THREADS;
+  // CTAs per SM asked of ptxas (register cap 64K / (THREADS * MINB))
+#ifndef TB_MINB
+#define TB_MINB 3
+#endif
+  static constexpr int MINB = THREADS <= 256 ? TB_MINB : 1;
 };
 
 // ---------------------------------------------------------------------------
 // K1: radial kernel (fused ramp when npad == L)
 // ---------------------------------------------------------------------------
 template <int L, bool RAMP>
-__global__ void __launch_bounds__(KShape<L>::THREADS) k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   extern __shared__ float2 smem[];
@@ -503,7 +508,7 @@ __device__ __forceinline__ size_t col_index(int H, int m2, int a) {
 // K2: gather + IFFT along k2 for one Cartesian column a in [0, H]
 // ---------------------------------------------------------------------------
 template <int L, bool CROP_HALF>
-__global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work w) {
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k2_columns(DevPlan p, Work w) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   constexpr int H = L / 2;
@@ -532,6 +537,7 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
       e[i] = active ? __ldg(tab + (size_t)a * (H + 1) + ab) : make_uint2(0xFFFFu, 0u);
     }
     const int V = p.n_theta;
+    const float2 m_t = (p.has_mod && active) ? __ldg(p.modt + t) : make_float2(1.f, 0.f);
     constexpr int NB = 4;
 #pragma unroll
     for (int c = 0; c < RPT; c += NB) {
@@ -554,12 +560,16 @@ __global__ void __launch_bounds__(KShape<L>::THREADS) k2_columns(DevPlan p, Work
           qt = qt ? 65536 - qt : 0;
         }
         const float2* row0 = pol + (size_t)t0 * H;
-        p00[j] = __ldg(row0 + ra);
-        p01[j] = __ldg(row0 + rb);
-        p10[j] = __ldg(row0 + H + ra);
-        p11[j] = __ldg(row0 + H + rb);
-        cc[j] = __ldg(com2 + ra);
-        mb[j] = p.has_mod ? __ldg(p.modt + (bs & (L - 1))) : make_float2(1.f, 0.f);
+        const float2 z = make_float2(0.f, 0.f);
+        const bool in = r0 != 0xFFFF;  // no polar traffic for nodes outside the disc
+        p00[j] = in ? __ldg(row0 + ra) : z;
+        p01[j] = in ? __ldg(row0 + rb) : z;
+        p10[j] = in ? __ldg(row0 + H + ra) : z;
+        p11[j] = in ? __ldg(row0 + H + rb) : z;
+        cc[j] = in ? __ldg(com2 + ra) : z;
+        // M[b] = M[t] * M[TPF*i] (linear phase in the signed index): one
+        // per-thread load plus a warp-uniform one instead of a load per node
+        mb[j] = p.has_mod ? cmul(m_t, __ldg(p.modt + (c + j) * TPF)) : make_float2(1.f, 0.f);
         rf[j] = (float)(ej.y & 0xFFFFu) * (1.f / 65536.f);
         tf[j] = (float)qt * (1.f / 65536.f);
       }
@@ -643,7 +653,7 @@ __device__ __forceinline__ float coverage(float x1, float x2) {
 }
 
 template <int L, bool CROP_HALF>
-__global__ void __launch_bounds__(KShape<L>::THREADS) k3_rows(DevPlan p, Work w, float* __restrict__ img,
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k3_rows(DevPlan p, Work w, float* __restrict__ img,
                                                               float out_scale) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
