@@ -135,15 +135,22 @@ struct Launch {
            (size_t)(L / 2) * 4;
   }
   static size_t smem_fft() { return K::BUF * sizeof(float2); }
+  using K2 = tb::K2Shape<L>;
+  static size_t smem_k2() { return (size_t)K2::G * K::BUF * sizeof(float2); }
+  // columns per K2 CTA: one resident CTA per SM sweeping G columns at a time
+  static int k2_cols(const tb_plan* p) {
+    const int steps = ((p->H + 1 + K2::G - 1) / K2::G + 147) / 148;
+    return K2::G * std::max(1, steps);
+  }
 
   static int configure(const tb_plan* p) {
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
     TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     if constexpr (L >= 64) {
-      TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+      TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
       TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     }
     TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
@@ -184,10 +191,12 @@ struct Launch {
     mark(2, 1);
     const bool half = L >= 64 && 2 * p->n == L;
     mark(3, 0);
+    const int kc = k2_cols(p);
+    const dim3 g2((p->H + 1 + kc - 1) / kc, B);
     if (half)
-      tb::k2_columns<L, (L >= 64)><<<dim3(p->H + 1, B), K::THREADS, smem_fft(), st>>>(dp, w);
+      tb::k2_columns<L, (L >= 64)><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
     else
-      tb::k2_columns<L, false><<<dim3(p->H + 1, B), K::THREADS, smem_fft(), st>>>(dp, w);
+      tb::k2_columns<L, false><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
     mark(3, 1);
     mark(4, 0);
     if (half)

@@ -506,17 +506,14 @@ __device__ __forceinline__ size_t col_index(int H, int m2, int a) {
 
 // ---------------------------------------------------------------------------
 // K2: gather + IFFT along k2 for one Cartesian column a in [0, H]
+// (device body; every thread of the CTA must call it -- FFT barriers)
 // ---------------------------------------------------------------------------
 template <int L, bool CROP_HALF>
-__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k2_columns(DevPlan p, Work w) {
+__device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a, int q, int t, bool active,
+                                          float2* smem) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   constexpr int H = L / 2;
-  extern __shared__ float2 smem[];
-  const int t = threadIdx.x;
-  const bool active = t < TPF;
-  const int a = blockIdx.x;
-  const int q = blockIdx.y;
   const int as = a < H ? a : -H;
   const float2* pol = w.polar + (size_t)q * p.prow * H;
   const float2* com = w.common + (size_t)q * H;
@@ -640,6 +637,37 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k2_column
       const bool keep = CROP_HALF ? (i < RPT / 4 || i >= 3 * RPT / 4) : (m2 < p.n);
       if (keep) out[col_index(H, m2, a)] = v[i];
     }
+  }
+}
+
+// K2 kernel: CTA of G column groups (G*TPF = 512 threads for L <= 8192)
+// sweeping a contiguous run of columns G at a time.  Adjacent columns read
+// nearly the same polar lines, so the SM's L1 keeps the shared footprint of
+// the G concurrent columns and of the next step resident.
+template <int L>
+struct K2Shape {
+  static constexpr int TPF = FftShape<L>::TPF;
+  static constexpr int G = TPF >= 512 ? 1 : 512 / TPF;
+  static constexpr int THREADS = G * TPF;
+};
+
+template <int L, bool CROP_HALF>
+__global__ void __launch_bounds__(K2Shape<L>::THREADS, 1) k2_columns(DevPlan p, Work w, int cols_per_cta) {
+  using K2 = K2Shape<L>;
+  constexpr int TPF = K2::TPF;
+  constexpr int H = L / 2;
+  extern __shared__ float2 smem[];
+  const int g = threadIdx.x / TPF;
+  const int t = threadIdx.x % TPF;
+  float2* buf = smem + g * KShape<L>::BUF;
+  const int q = blockIdx.y;
+  const int c0 = blockIdx.x * cols_per_cta;
+  const int c1 = min(H + 1, c0 + cols_per_cta);
+  for (int base = c0; base < c1; base += K2::G) {
+    const int a = base + g;
+    const bool valid = a < c1;
+    k2_column<L, CROP_HALF>(p, w, valid ? a : c1 - 1, q, t, valid, buf);
+    __syncthreads();  // buffer reuse by the next column
   }
 }
 
