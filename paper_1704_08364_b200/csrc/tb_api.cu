@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/tb_bst.h"
@@ -56,7 +57,7 @@ double bessel_i0(double x) {
   return sum;
 }
 
-size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+size_t align_up(size_t x) { return (x + 511) & ~(size_t)511; }  // textureAlignment
 
 }  // namespace
 
@@ -69,6 +70,15 @@ struct tb_plan {
   DevPlan dp;
   void* blob = nullptr;   // all small device tables in one allocation
   void* table = nullptr;  // gridding table [(H+1)^2] uint2
+  // texture objects over workspace polar regions, keyed by (pointer, rows);
+  // kept until the plan is destroyed (kernels may still be using them)
+  struct Tex {
+    const void* ptr;
+    int rows;
+    cudaTextureObject_t obj;
+  };
+  mutable std::mutex tex_mu;
+  mutable std::vector<Tex> texs;
 };
 
 namespace {
@@ -102,6 +112,8 @@ Layout layout_for(const tb_plan* p, int B) {
   return l;
 }
 
+cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows);
+
 Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   Layout l = layout_for(p, B);
   char* base = static_cast<char*>(ws) + (size_t)lane * l.lane_bytes;
@@ -117,7 +129,38 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   w.status = reinterpret_cast<int*>(static_cast<char*>(ws) + l.status);
   w.groups = p->groups;
   w.pairs_per_cta = p->pairs_per_cta;
+  w.polar_tex = polar_texture(p, w.polar, B * p->dp.prow);
   return w;
+}
+
+// Texture object viewing `rows` polar rows of H float2 texels at `ptr`
+// (0 when the view does not fit the device's pitch-2D limits).
+cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
+  if (p->desc.full_turn || p->desc.interp != TB_INTERP_BILINEAR) return 0;
+  if (rows > 65000 || p->H > 65000) return 0;
+  std::lock_guard<std::mutex> lk(p->tex_mu);
+  for (const auto& t : p->texs)
+    if (t.ptr == ptr && t.rows == rows) return t.obj;
+  cudaResourceDesc res{};
+  res.resType = cudaResourceTypePitch2D;
+  res.res.pitch2D.devPtr = const_cast<void*>(ptr);
+  res.res.pitch2D.desc = cudaCreateChannelDesc<float2>();
+  res.res.pitch2D.width = (size_t)p->H;
+  res.res.pitch2D.height = (size_t)rows;
+  res.res.pitch2D.pitchInBytes = (size_t)p->H * sizeof(float2);
+  cudaTextureDesc td{};
+  td.addressMode[0] = cudaAddressModeClamp;
+  td.addressMode[1] = cudaAddressModeClamp;
+  td.filterMode = cudaFilterModePoint;
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  cudaTextureObject_t obj = 0;
+  if (cudaCreateTextureObject(&obj, &res, &td, nullptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  p->texs.push_back({ptr, rows, obj});
+  return obj;
 }
 
 // ---------------------------------------------------------------------------
@@ -631,6 +674,7 @@ int tb_plan_destroy(tb_plan* p) {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
+    for (auto& t : p->texs) cudaDestroyTextureObject(t.obj);
     cudaFree(p->blob);
     if (p->table) cudaFree(p->table);
     if (prev >= 0) cudaSetDevice(prev);

@@ -62,6 +62,9 @@ struct Work {
   int* status;  // [0] non-finite input, [1] non-finite output
   int groups;   // K1 CTAs per slice (partial-sum groups)
   int pairs_per_cta;
+  // texture view of this lane's polar region (pitch 2D, float2 texels,
+  // width H, height B*(V+1)); 0 = use plain loads
+  cudaTextureObject_t polar_tex;
 };
 
 template <int L>
@@ -556,13 +559,29 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           t0 = qt ? V - I - 1 : V - I;
           qt = qt ? 65536 - qt : 0;
         }
-        const float2* row0 = pol + (size_t)t0 * H;
         const float2 z = make_float2(0.f, 0.f);
         const bool in = r0 != 0xFFFF;  // no polar traffic for nodes outside the disc
-        p00[j] = in ? __ldg(row0 + ra) : z;
-        p01[j] = in ? __ldg(row0 + rb) : z;
-        p10[j] = in ? __ldg(row0 + H + ra) : z;
-        p11[j] = in ? __ldg(row0 + H + rb) : z;
+        if (w.polar_tex) {
+          // one 2x2 texel gather per component (TLD4, point sampling: exact
+          // fp32 texels; the bilinear weights stay in fp32 below).  Texel
+          // (u, v) = (r, t); clamp addressing reproduces min(r0 + 1, H - 1).
+          const float fx = (float)(ra + 1), fy = (float)(q * (p.n_theta + 1) + t0 + 1);
+          float4 re = make_float4(0.f, 0.f, 0.f, 0.f), im = re;
+          if (in) {
+            re = tex2Dgather<float4>(w.polar_tex, fx, fy, 0);
+            im = tex2Dgather<float4>(w.polar_tex, fx, fy, 1);
+          }
+          p00[j] = make_float2(re.w, im.w);  // (u0, v0) = (ra, t0)
+          p01[j] = make_float2(re.z, im.z);  // (u1, v0) = (rb, t0)
+          p10[j] = make_float2(re.x, im.x);  // (u0, v1) = (ra, t0 + 1)
+          p11[j] = make_float2(re.y, im.y);  // (u1, v1) = (rb, t0 + 1)
+        } else {
+          const float2* row0 = pol + (size_t)t0 * H;
+          p00[j] = in ? __ldg(row0 + ra) : z;
+          p01[j] = in ? __ldg(row0 + rb) : z;
+          p10[j] = in ? __ldg(row0 + H + ra) : z;
+          p11[j] = in ? __ldg(row0 + H + rb) : z;
+        }
         cc[j] = in ? __ldg(com2 + ra) : z;
         // M[b] = M[t] * M[TPF*i] (linear phase in the signed index): one
         // per-thread load plus a warp-uniform one instead of a load per node
