@@ -560,17 +560,15 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           qt = qt ? 65536 - qt : 0;
         }
         const float2 z = make_float2(0.f, 0.f);
-        const bool in = r0 != 0xFFFF;  // no polar traffic for nodes outside the disc
+        const bool in = r0 != 0xFFFF;  // nodes outside the disc are masked below
         if (w.polar_tex) {
           // one 2x2 texel gather per component (TLD4, point sampling: exact
           // fp32 texels; the bilinear weights stay in fp32 below).  Texel
           // (u, v) = (r, t); clamp addressing reproduces min(r0 + 1, H - 1).
+          // Issued unconditionally (branch-free; outside nodes read r = 0).
           const float fx = (float)(ra + 1), fy = (float)(q * (p.n_theta + 1) + t0 + 1);
-          float4 re = make_float4(0.f, 0.f, 0.f, 0.f), im = re;
-          if (in) {
-            re = tex2Dgather<float4>(w.polar_tex, fx, fy, 0);
-            im = tex2Dgather<float4>(w.polar_tex, fx, fy, 1);
-          }
+          const float4 re = tex2Dgather<float4>(w.polar_tex, fx, fy, 0);
+          const float4 im = tex2Dgather<float4>(w.polar_tex, fx, fy, 1);
           p00[j] = make_float2(re.w, im.w);  // (u0, v0) = (ra, t0)
           p01[j] = make_float2(re.z, im.z);  // (u1, v0) = (rb, t0)
           p10[j] = make_float2(re.x, im.x);  // (u0, v1) = (ra, t0 + 1)
@@ -582,7 +580,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           p10[j] = in ? __ldg(row0 + H + ra) : z;
           p11[j] = in ? __ldg(row0 + H + rb) : z;
         }
-        cc[j] = in ? __ldg(com2 + ra) : z;
+        cc[j] = __ldg(com2 + ra);
         // M[b] = M[t] * M[TPF*i] (linear phase in the signed index): one
         // per-thread load plus a warp-uniform one instead of a load per node
         mb[j] = p.has_mod ? cmul(m_t, __ldg(p.modt + (c + j) * TPF)) : make_float2(1.f, 0.f);
@@ -695,8 +693,11 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, 1) k2_columns(DevPlan p, 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float coverage(float x1, float x2) {
   // fourier_bp.py:204-220 : pi inside the unit circle, 2 asin(1/r) outside
-  const float r = sqrtf(fmaf(x1, x1, x2 * x2));
-  return r > 1.f ? 2.f * asinf(1.f / r) : 3.14159265358979323846f;
+  // (asin only evaluated for the corner pixels)
+  const float r2 = fmaf(x1, x1, x2 * x2);
+  float c = 3.14159265358979323846f;
+  if (r2 > 1.f) c = 2.f * asinf(rsqrtf(r2));
+  return c;
 }
 
 template <int L, bool CROP_HALF>
