@@ -182,7 +182,8 @@ struct Launch {
   static size_t smem_k2() { return (size_t)K2::G * K::BUF * sizeof(float2); }
   // columns per K2 CTA: one resident CTA per SM sweeping G columns at a time
   static int k2_cols(const tb_plan* p) {
-    const int steps = ((p->H + 1 + K2::G - 1) / K2::G + 147) / 148;
+    const int resident = K2::THREADS <= 256 ? 2 : 1;  // CTAs per SM
+    const int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
     return K2::G * std::max(1, steps);
   }
 

@@ -664,12 +664,16 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
 template <int L>
 struct K2Shape {
   static constexpr int TPF = FftShape<L>::TPF;
-  static constexpr int G = TPF >= 512 ? 1 : 512 / TPF;
+#ifndef TB_K2_THREADS
+#define TB_K2_THREADS 256
+#endif
+  static constexpr int G = TPF >= TB_K2_THREADS ? 1 : TB_K2_THREADS / TPF;
   static constexpr int THREADS = G * TPF;
+  static constexpr int MINB = THREADS <= 256 ? 2 : 1;
 };
 
 template <int L, bool CROP_HALF>
-__global__ void __launch_bounds__(K2Shape<L>::THREADS, 1) k2_columns(DevPlan p, Work w, int cols_per_cta) {
+__global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_columns(DevPlan p, Work w, int cols_per_cta) {
   using K2 = K2Shape<L>;
   constexpr int TPF = K2::TPF;
   constexpr int H = L / 2;
