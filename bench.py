@@ -270,8 +270,8 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("kernel") == dom and tr.get("size") == n:
-            traffic = tr["dram_bytes_per_slice"] * slices_per_launch
+        if tr.get("size") == n and dom in tr.get("kernels", {}):
+            traffic = tr["kernels"][dom]["dram_bytes_per_slice"] * slices_per_launch
     except Exception:
         pass
     nat.read_status(ws)

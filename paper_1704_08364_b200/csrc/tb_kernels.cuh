@@ -309,10 +309,33 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
   const bool active = t < TPF;
   const int q = blockIdx.x;
   const float* part = w.part + (size_t)q * w.groups * p.S;
-  for (int i = t; i < p.S; i += blockDim.x) {
-    float s = 0.f;
-    for (int g = 0; g < w.groups; ++g) s += part[(size_t)g * p.S + i];
-    cs[i] = s;
+  {
+    // deterministic two-level sum over the K1 partial groups: warp wi sums
+    // groups wi, wi + nw, ... (independent loads in flight) into the FFT buffer,
+    // then a fixed-order sum over the nw warp partials
+    float* wsum = reinterpret_cast<float*>(buf);
+    const int nw = max(1, min((int)(blockDim.x >> 5), (2 * K::BUF) / max(p.S, 1)));
+    const int wi = t >> 5, lane = t & 31;
+    if (wi < nw) {
+      for (int i = lane; i < p.S; i += 32) {
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int g = wi;
+        for (; g + 3 * nw < w.groups; g += 4 * nw) {
+          s0 += __ldg(part + (size_t)g * p.S + i);
+          s1 += __ldg(part + (size_t)(g + nw) * p.S + i);
+          s2 += __ldg(part + (size_t)(g + 2 * nw) * p.S + i);
+          s3 += __ldg(part + (size_t)(g + 3 * nw) * p.S + i);
+        }
+        for (; g < w.groups; g += nw) s0 += __ldg(part + (size_t)g * p.S + i);
+        wsum[wi * p.S + i] = (s0 + s1) + (s2 + s3);
+      }
+    }
+    __syncthreads();
+    for (int i = t; i < p.S; i += blockDim.x) {
+      float s = 0.f;
+      for (int k = 0; k < nw; ++k) s += wsum[k * p.S + i];
+      cs[i] = s;
+    }
   }
   __syncthreads();
   float csum = 0.f;
