@@ -8,32 +8,23 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <mutex>
 #include <vector>
 
+#define TB_API_KERNELS
 #include "../../include/tb_bst.h"
 #include "tb_kernels.cuh"
+#include "tb_launch.cuh"
 
 using tb::DevPlan;
 using tb::Work;
 
+thread_local std::string tb_g_err;
+
 namespace {
-
-thread_local std::string g_err;
-
-int fail(int code, const std::string& msg) {
-  g_err = msg;
-  return code;
-}
-
-#define TB_CUDA(call)                                                                       \
-  do {                                                                                      \
-    cudaError_t e_ = (call);                                                                \
-    if (e_ != cudaSuccess)                                                                  \
-      return fail(TB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
-  } while (0)
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kMaxL = 8192;
@@ -58,32 +49,19 @@ double bessel_i0(double x) {
 }
 
 size_t align_up(size_t x) { return (x + 511) & ~(size_t)511; }  // textureAlignment
-
 }  // namespace
-
-struct tb_plan {
-  tb_plan_desc desc;
-  int device;
-  int n_t, V, rows, L, H, n, npad, lo, hi, S;
-  double amp;
-  int groups, pairs_per_cta;
-  DevPlan dp;
-  void* blob = nullptr;   // all small device tables in one allocation
-  void* table = nullptr;  // gridding table [(H+1)^2] uint2
-  // texture objects over workspace polar regions, keyed by (pointer, rows);
-  // kept until the plan is destroyed (kernels may still be using them)
-  struct Tex {
-    const void* ptr;
-    int rows;
-    cudaTextureObject_t obj;
-  };
-  mutable std::mutex tex_mu;
-  mutable std::vector<Tex> texs;
-};
 
 namespace {
 
-constexpr int kLanes = 2;  // concurrent launch groups (streams) per call
+// concurrent launch groups (streams) per call; TB_LANES overrides (tuning)
+int lanes_cfg() {
+  static const int v = [] {
+    const char* e = std::getenv("TB_LANES");
+    const int x = e ? std::atoi(e) : 0;
+    return (x >= 1 && x <= 8) ? x : 2;
+  }();
+  return v;
+}
 
 struct Layout {
   size_t polar, rowcoef, part, common, common2, coefmean, columns, filtered, status, total;
@@ -108,7 +86,7 @@ Layout layout_for(const tb_plan* p, int B) {
   l.columns = take((size_t)B * p->dp.col_slice * sizeof(float2));
   l.filtered = take((size_t)B * p->rows * p->n_t * sizeof(float));
   l.lane_bytes = off - l.polar;
-  l.total = off + (kLanes - 1) * l.lane_bytes;
+  l.total = off + (size_t)(lanes_cfg() - 1) * l.lane_bytes;
   return l;
 }
 
@@ -138,6 +116,7 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
 cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
   if (p->desc.full_turn || p->desc.interp != TB_INTERP_BILINEAR) return 0;
   if (rows > 65000 || p->H > 65000) return 0;
+  if (const char* e = std::getenv("TB_NOTEX")) if (std::atoi(e) == 1) return 0;  // A/B: plain gathers
   std::lock_guard<std::mutex> lk(p->tex_mu);
   for (const auto& t : p->texs)
     if (t.ptr == ptr && t.rows == rows) return t.obj;
@@ -163,112 +142,13 @@ cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
   return obj;
 }
 
-// ---------------------------------------------------------------------------
-// per-L launchers
-// ---------------------------------------------------------------------------
-template <int L>
-struct Launch {
-  using K = tb::KShape<L>;
-  static size_t smem_k1(const tb_plan* p) {
-    // FFT buffer + support sums + two TMA staging slots of a row pair + 2 mbarriers
-    return K::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 + (size_t)4 * p->n_t * 4 + 16;
-  }
-  static size_t smem_k1b(const tb_plan* p) {
-    return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::K1B_THREADS * 4 +
-           (size_t)(L / 2) * 4;
-  }
-  static size_t smem_fft() { return K::BUF * sizeof(float2); }
-  using K2 = tb::K2Shape<L>;
-  static size_t smem_k2() { return (size_t)K2::G * K::BUF * sizeof(float2); }
-  // columns per K2 CTA: one resident CTA per SM sweeping G columns at a time
-  static int k2_cols(const tb_plan* p) {
-    const int resident = K2::THREADS <= 256 ? 2 : 1;  // CTAs per SM
-    const int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
-    return K2::G * std::max(1, steps);
-  }
-
-  static int configure(const tb_plan* p) {
-    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
-    TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
-    if constexpr (L >= 64) {
-      TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
-      TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
-    }
-    TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
-    return TB_OK;
-  }
-
-  // one launch group of B slices through K1 -> K1b -> K2 -> K3.  `ev`, when
-  // given, receives start/stop events around each stage: [stage][2] with
-  // stages 0 ramp (unfused path), 1 K1, 2 K1b, 3 K2, 4 K3.
-  static int bst_group(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp,
-                       float out_scale, cudaStream_t st, cudaEvent_t* ev) {
-    const DevPlan& dp = p->dp;
-    const float* k1_in = sino;
-    bool fused = false;
-    auto mark = [&](int stage, int which) {
-      if (ev) cudaEventRecord(ev[2 * stage + which], st);
-    };
-    if (ramp) {
-      if (p->npad == L) {
-        fused = true;
-      } else {
-        mark(0, 0);
-        int rc = ramp_rows(p, sino, w.filtered, B * p->rows, w, st);
-        mark(0, 1);
-        if (rc) return rc;
-        k1_in = w.filtered;
-      }
-    }
-    dim3 g1(p->groups, B);
-    mark(1, 0);
-    if (fused)
-      tb::k1_radial<L, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
-    else
-      tb::k1_radial<L, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
-    mark(1, 1);
-    mark(2, 0);
-    tb::k1b_common<L><<<B, K::K1B_THREADS, smem_k1b(p), st>>>(dp, w);
-    mark(2, 1);
-    const bool half = L >= 64 && 2 * p->n == L;
-    mark(3, 0);
-    const int kc = k2_cols(p);
-    const dim3 g2((p->H + 1 + kc - 1) / kc, B);
-    if (half)
-      tb::k2_columns<L, (L >= 64)><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
-    else
-      tb::k2_columns<L, false><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
-    mark(3, 1);
-    mark(4, 0);
-    if (half)
-      tb::k3_rows<L, (L >= 64)><<<dim3((p->n + 3) / 4, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
-    else
-      tb::k3_rows<L, false><<<dim3((p->n + 3) / 4, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
-    mark(4, 1);
-    TB_CUDA(cudaGetLastError());
-    return TB_OK;
-  }
-
-  static int ramp_rows(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,
-                       cudaStream_t st);
-};
-
-template <int NP>
-int launch_ramp(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
-  using K = tb::KShape<NP>;
-  tb::kr_ramp<NP><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);
-  TB_CUDA(cudaGetLastError());
-  return TB_OK;
-}
+}  // namespace
 
 int ramp_dispatch(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
   switch (p->npad) {
 #define TB_CASE(N) \
   case N:          \
-    return launch_ramp<N>(p, in, out, total_rows, w, st);
+    return tb_ramp_##N(p, in, out, total_rows, w, st);
     TB_CASE(4) TB_CASE(8) TB_CASE(16) TB_CASE(32) TB_CASE(64) TB_CASE(128) TB_CASE(256) TB_CASE(512)
     TB_CASE(1024) TB_CASE(2048) TB_CASE(4096) TB_CASE(8192)
 #undef TB_CASE
@@ -276,34 +156,21 @@ int ramp_dispatch(const tb_plan* p, const float* in, float* out, int total_rows,
   return fail(TB_ERR_UNSUPPORTED, "ramp length not supported on the GPU path");
 }
 
-template <int L>
-int Launch<L>::ramp_rows(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,
-                         cudaStream_t st) {
-  return ramp_dispatch(p, in, out, total_rows, w, st);
-}
 
-#define TB_DISPATCH_L(Lval, EXPR_TEMPLATE)                                                   \
-  switch (Lval) {                                                                           \
-    case 4: { constexpr int L_ = 4; return EXPR_TEMPLATE; }                                 \
-    case 8: { constexpr int L_ = 8; return EXPR_TEMPLATE; }                                 \
-    case 16: { constexpr int L_ = 16; return EXPR_TEMPLATE; }                               \
-    case 32: { constexpr int L_ = 32; return EXPR_TEMPLATE; }                               \
-    case 64: { constexpr int L_ = 64; return EXPR_TEMPLATE; }                               \
-    case 128: { constexpr int L_ = 128; return EXPR_TEMPLATE; }                             \
-    case 256: { constexpr int L_ = 256; return EXPR_TEMPLATE; }                             \
-    case 512: { constexpr int L_ = 512; return EXPR_TEMPLATE; }                             \
-    case 1024: { constexpr int L_ = 1024; return EXPR_TEMPLATE; }                           \
-    case 2048: { constexpr int L_ = 2048; return EXPR_TEMPLATE; }                           \
-    case 4096: { constexpr int L_ = 4096; return EXPR_TEMPLATE; }                           \
-    case 8192: { constexpr int L_ = 8192; return EXPR_TEMPLATE; }                           \
-  }                                                                                         \
+namespace {
+
+#define TB_CASE_CFG(N) case N: return tb_configure_##N(p);
+#define TB_CASE_GRP(N) case N: return tb_group_##N(p, sino, img, B, w, ramp, scale, st, ev);
+
+int configure_dispatch(tb_plan* p) {
+  switch (p->L) { TB_FOR_EACH_L(TB_CASE_CFG) }
   return fail(TB_ERR_UNSUPPORTED, "radial_samples not supported on the GPU path");
-
-int configure_dispatch(const tb_plan* p) { TB_DISPATCH_L(p->L, Launch<L_>::configure(p)) }
+}
 
 int bst_dispatch(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp, float scale,
                  cudaStream_t st, cudaEvent_t* ev = nullptr) {
-  TB_DISPATCH_L(p->L, Launch<L_>::bst_group(p, sino, img, B, w, ramp, scale, st, ev))
+  switch (p->L) { TB_FOR_EACH_L(TB_CASE_GRP) }
+  return fail(TB_ERR_UNSUPPORTED, "radial_samples not supported on the GPU path");
 }
 
 int check_exec_args(const tb_plan* p, const void* a, const void* b, int n_slices, int batch, const void* ws,
@@ -345,35 +212,41 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
     evs.resize((size_t)ngroups * 10);
     for (auto& e : evs) TB_CUDA(cudaEventCreate(&e));
   }
-  // two lanes: launch group g runs on lane g % 2 (the caller's stream and an
-  // auxiliary stream forked from it), each lane with its own workspace region,
-  // so one group's serial K1b / kernel tails overlap the other group's work.
-  // The profiled variant stays on one lane so per-kernel times are clean.
-  const int lanes = (stage_ms || ngroups < 2) ? 1 : kLanes;
-  cudaStream_t aux = nullptr;
+  // lanes: launch group g runs on lane g % lanes (lane 0 = the caller's
+  // stream, the others auxiliary streams forked from it), each lane with its
+  // own workspace region, so one group's serial K1b / kernel tails overlap
+  // the other groups' work.  The profiled variant stays on one lane so
+  // per-kernel times are clean.
+  const int lanes = (stage_ms || ngroups < 2) ? 1 : std::min(lanes_cfg(), ngroups);
+  cudaStream_t aux[8] = {};
   cudaEvent_t fork = nullptr, join = nullptr;
   if (lanes > 1) {
-    TB_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
     TB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     TB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
     TB_CUDA(cudaEventRecord(fork, st));
-    TB_CUDA(cudaStreamWaitEvent(aux, fork, 0));
+    for (int l = 1; l < lanes; ++l) {
+      TB_CUDA(cudaStreamCreateWithFlags(&aux[l], cudaStreamNonBlocking));
+      TB_CUDA(cudaStreamWaitEvent(aux[l], fork, 0));
+    }
   }
   for (int g = 0; g < ngroups; ++g) {
     const int s0 = g * batch;
     const int B = std::min(batch, n_slices - s0);
     const int lane = g % lanes;
     Work w = work_for(p, batch, ws, lane);
-    rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, lane ? aux : st,
+    cudaStream_t ls = lane ? aux[lane] : st;
+    rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, ls,
                       stage_ms ? evs.data() + (size_t)g * 10 : nullptr);
     if (rc) break;
   }
   if (lanes > 1) {
-    cudaEventRecord(join, aux);
-    cudaStreamWaitEvent(st, join, 0);
+    for (int l = 1; l < lanes; ++l) {
+      cudaEventRecord(join, aux[l]);
+      cudaStreamWaitEvent(st, join, 0);
+      cudaStreamDestroy(aux[l]);  // released once its queued work completes
+    }
     cudaEventDestroy(fork);
     cudaEventDestroy(join);
-    cudaStreamDestroy(aux);  // released once its queued work completes
   }
   if (stage_ms) {
     if (!rc) {
@@ -402,7 +275,7 @@ extern "C" {
 
 int tb_abi_version(void) { return TB_ABI_VERSION; }
 
-const char* tb_last_error(void) { return g_err.c_str(); }
+const char* tb_last_error(void) { return tb_g_err.c_str(); }
 
 int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   if (!d || !out) return fail(TB_ERR_INVALID, "null argument");
@@ -642,7 +515,8 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   dp.psi = reinterpret_cast<const float2*>(b + o_psi);
   dp.rho = reinterpret_cast<const float2*>(b + o_rho);
   dp.modt = reinterpret_cast<const float2*>(b + o_mod);
-  dp.col_slice = (size_t)((n + 3) / 4) * (H + 1) * 4;
+  // per-slice K2 output padded to 128 B: slices never share a cache line
+  dp.col_slice = (((size_t)((n + 3) / 4) * (H + 1) * 4 + 15) / 16) * 16;
   dp.prow = d->full_turn ? 2 * V : V + 1;
   dp.ss_cs = reinterpret_cast<const double2*>(b + o_ss);
 
@@ -661,7 +535,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
 
   int rc = configure_dispatch(p);
   if (rc) {
-    std::string m = g_err;
+    std::string m = tb_g_err;
     return cleanup(rc, m);
   }
   if (prev >= 0 && prev != device) cudaSetDevice(prev);

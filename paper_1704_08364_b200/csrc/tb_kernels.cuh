@@ -294,12 +294,13 @@ __global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const 
 // ---------------------------------------------------------------------------
 // K1b: common (angle-independent) row and coef.mean() per slice
 // ---------------------------------------------------------------------------
+// smem: [BUF float2][S][S][2 blockDim][H] floats.  The K1 partials are read
+// through L2 (__ldcg): touched once, no reuse for L1.
 template <int L>
-__global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, Work w) {
+__device__ __forceinline__ void k1b_slice(const DevPlan& p, const Work& w, int q, float2* smem) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   constexpr int H = L / 2;
-  extern __shared__ float2 smem[];
   float2* buf = smem;
   float* cs = reinterpret_cast<float*>(smem + K::BUF);
   float* bm = cs + p.S;
@@ -307,8 +308,8 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
   float* buf2 = red + 2 * blockDim.x;  // [H] real part of the common row
   const int t = threadIdx.x;
   const bool active = t < TPF;
-  const int q = blockIdx.x;
   const float* part = w.part + (size_t)q * w.groups * p.S;
+  __syncthreads();  // smem of the previous item released
   {
     // deterministic two-level sum over the K1 partial groups: warp wi sums
     // groups wi, wi + nw, ... (independent loads in flight) into the FFT buffer,
@@ -321,12 +322,12 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         int g = wi;
         for (; g + 3 * nw < w.groups; g += 4 * nw) {
-          s0 += __ldg(part + (size_t)g * p.S + i);
-          s1 += __ldg(part + (size_t)(g + nw) * p.S + i);
-          s2 += __ldg(part + (size_t)(g + 2 * nw) * p.S + i);
-          s3 += __ldg(part + (size_t)(g + 3 * nw) * p.S + i);
+          s0 += __ldcg(part + (size_t)g * p.S + i);
+          s1 += __ldcg(part + (size_t)(g + nw) * p.S + i);
+          s2 += __ldcg(part + (size_t)(g + 2 * nw) * p.S + i);
+          s3 += __ldcg(part + (size_t)(g + 3 * nw) * p.S + i);
         }
-        for (; g < w.groups; g += nw) s0 += __ldg(part + (size_t)g * p.S + i);
+        for (; g < w.groups; g += nw) s0 += __ldcg(part + (size_t)g * p.S + i);
         wsum[wi * p.S + i] = (s0 + s1) + (s2 + s3);
       }
     }
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
   }
   // rect coefficient of the common row and mean of the per-row coefficients
   float asum = 0.f;
-  for (int j = t; j < p.rows; j += blockDim.x) asum += w.rowcoef[(size_t)q * p.rows + j];
+  for (int j = t; j < p.rows; j += blockDim.x) asum += __ldcg(w.rowcoef + (size_t)q * p.rows + j);
   red[t] = csum;
   red[t + blockDim.x] = asum;
   __syncthreads();
@@ -392,6 +393,12 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
   for (int k = t; k < H; k += blockDim.x) out2[k] = make_float2(buf2[k], buf2[min(k + 1, H - 1)]);
 }
 
+template <int L>
+__global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, Work w) {
+  extern __shared__ float2 smem[];
+  k1b_slice<L>(p, w, blockIdx.x, smem);
+}
+
 // ---------------------------------------------------------------------------
 // gridding table (fourier_bp.py:222-249): built once per plan in fp64.
 // One entry per first-quadrant lattice node (|a|, |b|) in [0, H]^2, stored
@@ -401,6 +408,7 @@ __global__ void __launch_bounds__(KShape<L>::K1B_THREADS) k1b_common(DevPlan p, 
 // with ri = hypot(nu1, nu2)/df and tq = atan2(|nu2|, |nu1|) * 2V / (2 pi).
 // The quantised fractions carry <= 2^-17 absolute weight error.
 // ---------------------------------------------------------------------------
+#ifdef TB_API_KERNELS  // non-template kernels: emitted by tb_api.cu only
 __global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab, int H, double dnu, double df,
                                                         double tscale, int nearest) {
   const long long count = (long long)(H + 1) * (H + 1);
@@ -428,6 +436,7 @@ __global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab,
   e.y = (uint32_t)qr | ((uint32_t)qt << 16);
   tab[i] = e;
 }
+#endif
 
 // polar sample P(t, r) of the full circle; rows t >= V of half-turn input are
 // the conjugate mirror (fourier_bp.py:302-311; SURVEY.md finding 2)
@@ -534,9 +543,21 @@ __device__ __forceinline__ size_t col_index(int H, int m2, int a) {
 // K2: gather + IFFT along k2 for one Cartesian column a in [0, H]
 // (device body; every thread of the CTA must call it -- FFT barriers)
 // ---------------------------------------------------------------------------
+// table entry, streamed past L1 (read once per column; keeps L1 for polar texels)
+__device__ __forceinline__ uint2 ld_table(const uint2* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+// Finished nodes are staged in the FFT buffer (thread-private slots: node i
+// of thread t at smem[i * TPF + t]) so they leave registers during the
+// latency-bound gather; a barrier separates the reload from the first FFT
+// pass, which rewrites the buffer.
 template <int L, bool CROP_HALF>
 __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a, int q, int t, bool active,
                                           float2* smem) {
+  float2* stg = smem;
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   constexpr int H = L / 2;
@@ -549,28 +570,46 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     // Half-turn bilinear fast path.  A node in the lower half plane (b < 0)
     // is the conjugate of its point reflection (-a, -b), which lies in the
     // upper half plane and reads polar rows t in [0, V] (row V = conj row 0):
-    // no per-corner mirror logic.  Software-pipelined: all table entries
-    // first, then the corner gathers of NB nodes at a time.
+    // no per-corner mirror logic.  Groups of NB nodes: the table entries of
+    // the next group load while this group's corners are gathered.
     const float2* com2 = w.common2 + (size_t)q * H;
-    uint2 e[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int b = t + i * TPF;
-      const int ab = b <= H ? b : L - b;
-      e[i] = active ? __ldg(tab + (size_t)a * (H + 1) + ab) : make_uint2(0xFFFFu, 0u);
-    }
+    const uint2* trow = tab + (size_t)a * (H + 1);
     const int V = p.n_theta;
-    const float2 m_t = (p.has_mod && active) ? __ldg(p.modt + t) : make_float2(1.f, 0.f);
-    constexpr int NB = 4;
+    // M[a] M[b] with M[b] = M[t] M[TPF i]: the column factor M[a] folds into
+    // the per-thread factor once per column
+    const float2 m_t = (p.has_mod && active) ? cmul(__ldg(p.modt + t), __ldg(p.modt + (as & (L - 1))))
+                                             : make_float2(1.f, 0.f);
+#ifndef TB_K2_NB
+#define TB_K2_NB 4
+#endif
+    constexpr int NB = TB_K2_NB < RPT ? TB_K2_NB : RPT;
+    uint2 en[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int b = t + j * TPF;
+      const int ab = b <= H ? b : L - b;
+      en[j] = active ? ld_table(trow + ab) : make_uint2(0xFFFFu, 0u);
+    }
 #pragma unroll
     for (int c = 0; c < RPT; c += NB) {
+      uint2 e[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) e[j] = en[j];
+      if (c + NB < RPT) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int b = t + (c + NB + j) * TPF;
+          const int ab = b <= H ? b : L - b;
+          en[j] = active ? ld_table(trow + ab) : make_uint2(0xFFFFu, 0u);
+        }
+      }
       float2 p00[NB], p01[NB], p10[NB], p11[NB], cc[NB], mb[NB];
       float rf[NB], tf[NB];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const int b = t + (c + j) * TPF;
         const int bs = b < H ? b : b - L;
-        const uint2 ej = e[c + j];
+        const uint2 ej = e[j];
         const int r0 = (int)(ej.x & 0xFFFFu);
         const int ra = r0 == 0xFFFF ? 0 : r0;
         const int rb = min(ra + 1, H - 1);
@@ -621,15 +660,13 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
                                  fmaf(u, r1v.y - r0v.y, r0v.y));
         if (lower) val.y = -val.y;
         if (p.has_mod) val = cmul(val, mb[j]);
-        v[c + j] = ((e[c + j].x & 0xFFFFu) == 0xFFFFu) ? make_float2(0.f, 0.f) : val;
+        if (active) stg[(c + j) * TPF + t] = ((e[j].x & 0xFFFFu) == 0xFFFFu) ? make_float2(0.f, 0.f) : val;
       }
     }
     if (p.nyq && active) {
       // Nyquist lines: Hermitian part 0.5 (C[k] + conj C[-k mod L]) of the fully
-      // modulated lattice (.real of ifft2, fourier_bp.py:431); the column
-      // factor M[a] is re-applied in K3, so divide it out here
-      const float2 ma = p.has_mod ? __ldg(p.modt + (as & (L - 1))) : make_float2(1.f, 0.f);
-#pragma unroll
+      // modulated lattice (.real of ifft2, fourier_bp.py:431)
+#pragma unroll 1
       for (int i = 0; i < RPT; ++i) {
         const int b = t + i * TPF;
         if (a == H || b == H) {
@@ -638,11 +675,13 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           const int pb = bs == -H ? -H : -bs;
           const float2 c0 = lattice_value(p, tab, pol, com, as, bs);
           const float2 m = lattice_value(p, tab, pol, com, pa, pb);
-          const float2 hv = make_float2(0.5f * (c0.x + m.x), 0.5f * (c0.y - m.y));
-          v[i] = cmul(hv, make_float2(ma.x, -ma.y));
+          stg[i * TPF + t] = make_float2(0.5f * (c0.x + m.x), 0.5f * (c0.y - m.y));
         }
       }
     }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) v[i] = active ? stg[i * TPF + t] : make_float2(0.f, 0.f);
+    __syncthreads();  // every thread holds its nodes before the FFT rewrites the buffer
   } else {
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -657,10 +696,6 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           const int pb = bs == -H ? -H : -bs;
           const float2 m = lattice_value(p, tab, pol, com, pa, pb);
           val = make_float2(0.5f * (val.x + m.x), 0.5f * (val.y - m.y));
-        }
-        if (p.has_mod) {  // K3 applies the column factor M[a]
-          const float2 ma = __ldg(p.modt + (as & (L - 1)));
-          val = cmul(val, make_float2(ma.x, -ma.y));
         }
       }
       v[i] = val;
@@ -692,7 +727,11 @@ struct K2Shape {
 #endif
   static constexpr int G = TPF >= TB_K2_THREADS ? 1 : TB_K2_THREADS / TPF;
   static constexpr int THREADS = G * TPF;
-  static constexpr int MINB = THREADS <= 256 ? 2 : 1;
+#ifndef TB_K2_MINB
+#define TB_K2_MINB 3
+#endif
+  static constexpr int MINB = THREADS <= 256 ? TB_K2_MINB : 1;
+  static constexpr int SMEM_PER_GROUP = KShape<L>::BUF;  // float2 FFT buffer (+ gather staging)
 };
 
 template <int L, bool CROP_HALF>
@@ -703,7 +742,7 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_colu
   extern __shared__ float2 smem[];
   const int g = threadIdx.x / TPF;
   const int t = threadIdx.x % TPF;
-  float2* buf = smem + g * KShape<L>::BUF;
+  float2* buf = smem + g * K2::SMEM_PER_GROUP;
   const int q = blockIdx.y;
   const int c0 = blockIdx.x * cols_per_cta;
   const int c1 = min(H + 1, c0 + cols_per_cta);
@@ -718,31 +757,27 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_colu
 // ---------------------------------------------------------------------------
 // K3: C2R along k1 for a tile of 4 output rows (two packed pairs) + epilogue
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float coverage(float x1, float x2) {
-  // fourier_bp.py:204-220 : pi inside the unit circle, 2 asin(1/r) outside
-  // (asin only evaluated for the corner pixels)
-  const float r2 = fmaf(x1, x1, x2 * x2);
-  float c = 3.14159265358979323846f;
-  if (r2 > 1.f) c = 2.f * asinf(rsqrtf(r2));
-  return c;
-}
 
+// One 4-row output tile (two packed row pairs) of the slice in workspace
+// slot q, written to img_slice [n][n].  The K2 columns
+// already carry the full half-node modulation M[a] M[b].  `chk` accumulates
+// out * 0 (NaN for any non-finite output) for the caller's status flag.
 template <int L, bool CROP_HALF>
-__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k3_rows(DevPlan p, Work w, float* __restrict__ img,
-                                                              float out_scale) {
+__device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* __restrict__ img_slice, float out_scale,
+                                        int q, int tile, float2* smem, float& chk) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   constexpr int H = L / 2;
-  extern __shared__ float2 smem[];
   const int t = threadIdx.x;
   const bool active = t < TPF;
-  const int tile = blockIdx.x;
-  const int q = blockIdx.y;
   const int n = p.n;
   const float2* G = w.columns + (size_t)q * p.col_slice + (size_t)tile * (H + 1) * 4;
-  const float cm = w.coefmean[q];
+  const float cm = __ldcg(w.coefmean + q);  // written by another CTA (K1b)
   const float inv_n = 2.f / (float)n;
-  bool bad = false;
+  const float A = p.img_scale * out_scale;       // amplitude / L^2 / (2 pi)
+  const float cmo = cm * out_scale;               // coef_mean / (2 pi)
+  const float Bpi = cmo * 3.14159265358979323846f;  // inside the unit circle
+  const float xt = fmaf((float)t, inv_n, 0.5f * inv_n - 1.f);  // x of column t (+ i TPF inv_n)
   for (int pair = 0; pair < 2; ++pair) {
     const int m2a = 4 * tile + 2 * pair, m2b = m2a + 1;
     if (m2a >= n) break;  // uniform across the CTA
@@ -752,18 +787,16 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k3_rows(D
     for (int i = 0; i < RPT; ++i) {
       float2 z = make_float2(0.f, 0.f);
       if (active) {
-        const int a = t + i * TPF;
-        const int ar = a <= H ? a : L - a;
+        // a = t + i TPF; bins a > H are the conjugates of L - a (i >= RPT/2)
+        const int ar = (i < RPT / 2) ? t + i * TPF : L - (t + i * TPF);
         const float4 g = __ldg(reinterpret_cast<const float4*>(G + (size_t)ar * 4 + 2 * pair));
         float2 ga = make_float2(g.x, g.y);
         float2 gb = hasb ? make_float2(g.z, g.w) : make_float2(0.f, 0.f);
-        if (p.has_mod) {  // column half-node factor M[a] (fourier_bp.py:430)
-          const float2 ma = __ldg(p.modt + ar);
-          ga = cmul(ga, ma);
-          gb = cmul(gb, ma);
+        if (i >= RPT / 2) { ga.y = -ga.y; gb.y = -gb.y; }
+        if (i == 0 || i == RPT / 2) {
+          // C2R ignores the imaginary part of the DC and Nyquist bins
+          if (t == 0) { ga.y = 0.f; gb.y = 0.f; }
         }
-        if (a == 0 || a == H) { ga.y = 0.f; gb.y = 0.f; }
-        if (a > H) { ga.y = -ga.y; gb.y = -gb.y; }
         z = make_float2(ga.x - gb.y, ga.y + gb.x);  // ga + i gb
       }
       v[i] = z;
@@ -772,34 +805,56 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k3_rows(D
     if (active) {
       const float x2a = -1.f + ((float)m2a + 0.5f) * inv_n;
       const float x2b = -1.f + ((float)m2b + 0.5f) * inv_n;
-      float* oa = img + ((size_t)q * n + m2a) * n;
+      float* oa = img_slice + (size_t)m2a * n;
       float* ob = oa + n;
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const int idx = t + i * TPF;
-        const int m1 = (idx + p.n_half) & (L - 1);
-        const bool keep = CROP_HALF ? (i < RPT / 4 || i >= 3 * RPT / 4) : (m1 < n);
+        int m1;
+        bool keep;
+        if constexpr (CROP_HALF) {
+          // n = L/2, offset L/4: rows i < RPT/4 -> m1 = idx + L/4,
+          // i >= 3 RPT/4 -> m1 = idx - 3L/4 (others cropped, DCE'd)
+          keep = i < RPT / 4 || i >= 3 * RPT / 4;
+          m1 = i < RPT / 4 ? idx + L / 4 : idx - 3 * L / 4;
+        } else {
+          m1 = (idx + p.n_half) & (L - 1);
+          keep = m1 < n;
+        }
         if (keep) {
-          const float x1 = -1.f + ((float)m1 + 0.5f) * inv_n;
-          const float ra = fmaf(v[i].x, p.img_scale, cm * coverage(x1, x2a)) * out_scale;
+          // x1 of output column m1 (coverage add-back, fourier_bp.py:204-220, 458)
+          const float x1 = CROP_HALF ? fmaf((float)(m1 - t), inv_n, xt) : -1.f + ((float)m1 + 0.5f) * inv_n;
+          float ra = fmaf(v[i].x, A, Bpi);
+          float rb = fmaf(v[i].y, A, Bpi);
+          const float r2a = fmaf(x1, x1, x2a * x2a), r2b = fmaf(x1, x1, x2b * x2b);
+          if (r2a > 1.f) ra += cmo * (2.f * asinf(rsqrtf(r2a)) - 3.14159265358979323846f);
+          if (r2b > 1.f) rb += cmo * (2.f * asinf(rsqrtf(r2b)) - 3.14159265358979323846f);
           oa[m1] = ra;
-          bad |= !isfinite(ra);
+          chk = fmaf(ra, 0.f, chk);
           if (hasb) {
-            const float rb = fmaf(v[i].y, p.img_scale, cm * coverage(x1, x2b)) * out_scale;
             ob[m1] = rb;
-            bad |= !isfinite(rb);
+            chk = fmaf(rb, 0.f, chk);
           }
         }
       }
     }
     __syncthreads();  // smem reuse by the next pair
   }
-  if (bad) atomicOr(&w.status[1], 1);
+}
+
+template <int L, bool CROP_HALF>
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k3_rows(DevPlan p, Work w, float* __restrict__ img,
+                                                              float out_scale) {
+  extern __shared__ float2 smem[];
+  float chk = 0.f;
+  k3_tile<L, CROP_HALF>(p, w, img + (size_t)blockIdx.y * p.n * p.n, out_scale, blockIdx.y, blockIdx.x, smem, chk);
+  if (chk != 0.f) atomicOr(&w.status[1], 1);
 }
 
 // ---------------------------------------------------------------------------
 // K5: slant-stack backprojection (projector.py:126-158)
 // ---------------------------------------------------------------------------
+#ifdef TB_API_KERNELS
 __global__ void __launch_bounds__(256) k5_slant(DevPlan p, const float* __restrict__ rows, int n_ang,
                                                 float* __restrict__ img, float scale, Work w) {
   const int m1 = blockIdx.x * 16 + (threadIdx.x & 15);
@@ -830,5 +885,6 @@ __global__ void __launch_bounds__(256) k5_slant(DevPlan p, const float* __restri
   img[((size_t)q * n + m2) * n + m1] = out;
   if (w.status && !isfinite(out)) atomicOr(&w.status[1], 1);
 }
+#endif
 
 }  // namespace tb

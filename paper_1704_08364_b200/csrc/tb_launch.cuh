@@ -1,0 +1,174 @@
+// tb_launch.cuh -- host-side per-L launchers shared by tb_api.cu (plan, ABI,
+// dispatch) and the per-L instantiation units tb_inst.cu (compiled once per
+// radial length with -DTB_L=<L>, so the sm_100a build parallelises).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tb_bst.h"
+#include "tb_kernels.cuh"
+
+using tb::DevPlan;
+using tb::Work;
+
+// last error message of the calling thread (defined in tb_api.cu)
+extern thread_local std::string tb_g_err;
+
+inline int fail(int code, const std::string& msg) {
+  tb_g_err = msg;
+  return code;
+}
+
+#define TB_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(TB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+struct tb_plan {
+  tb_plan_desc desc;
+  int device;
+  int n_t, V, rows, L, H, n, npad, lo, hi, S;
+  double amp;
+  int groups, pairs_per_cta;
+  DevPlan dp;
+  void* blob = nullptr;   // all small device tables in one allocation
+  void* table = nullptr;  // gridding table [(H+1)^2] uint2
+  // texture objects over workspace polar regions, keyed by (pointer, rows);
+  // kept until the plan is destroyed (kernels may still be using them)
+  struct Tex {
+    const void* ptr;
+    int rows;
+    cudaTextureObject_t obj;
+  };
+  mutable std::mutex tex_mu;
+  mutable std::vector<Tex> texs;
+};
+
+// ---------------------------------------------------------------------------
+// per-L launchers
+// ---------------------------------------------------------------------------
+template <int L>
+struct Launch {
+  using K = tb::KShape<L>;
+  static size_t smem_k1(const tb_plan* p) {
+    // FFT buffer + support sums + two TMA staging slots of a row pair + 2 mbarriers
+    return K::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 + (size_t)4 * p->n_t * 4 + 16;
+  }
+  static size_t smem_k1b(const tb_plan* p) {
+    return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::K1B_THREADS * 4 +
+           (size_t)(L / 2) * 4;
+  }
+  static size_t smem_fft() { return K::BUF * sizeof(float2); }
+  using K2 = tb::K2Shape<L>;
+  static size_t smem_k2() { return (size_t)K2::G * K2::SMEM_PER_GROUP * sizeof(float2); }
+  // columns per K2 CTA: one resident CTA per SM sweeping G columns at a time
+  static int k2_cols(const tb_plan* p) {
+    const int resident = K2::MINB;  // CTAs per SM
+    const int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
+    return K2::G * std::max(1, steps);
+  }
+
+  static int configure(tb_plan* p) {
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
+    TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    if constexpr (L >= 64) {
+      TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
+      TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    }
+    TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    return TB_OK;
+  }
+
+  // one launch group of B slices through K1 -> K1b -> K2 -> K3.  `ev`, when
+  // given, receives start/stop events around each stage: [stage][2] with
+  // stages 0 ramp (unfused path), 1 K1, 2 K1b, 3 K2, 4 K3.
+  static int bst_group(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp,
+                       float out_scale, cudaStream_t st, cudaEvent_t* ev) {
+    const DevPlan& dp = p->dp;
+    const float* k1_in = sino;
+    bool fused = false;
+    auto mark = [&](int stage, int which) {
+      if (ev) cudaEventRecord(ev[2 * stage + which], st);
+    };
+    if (ramp) {
+      if (p->npad == L) {
+        fused = true;
+      } else {
+        mark(0, 0);
+        int rc = ramp_rows(p, sino, w.filtered, B * p->rows, w, st);
+        mark(0, 1);
+        if (rc) return rc;
+        k1_in = w.filtered;
+      }
+    }
+    dim3 g1(p->groups, B);
+    mark(1, 0);
+    if (fused)
+      tb::k1_radial<L, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    else
+      tb::k1_radial<L, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    mark(1, 1);
+    mark(2, 0);
+    tb::k1b_common<L><<<B, K::K1B_THREADS, smem_k1b(p), st>>>(dp, w);
+    mark(2, 1);
+    const bool half = L >= 64 && 2 * p->n == L;
+    mark(3, 0);
+    const int kc = k2_cols(p);
+    const dim3 g2((p->H + 1 + kc - 1) / kc, B);
+    if (half)
+      tb::k2_columns<L, (L >= 64)><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
+    else
+      tb::k2_columns<L, false><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
+    mark(3, 1);
+    mark(4, 0);
+    if (half)
+      tb::k3_rows<L, (L >= 64)><<<dim3((p->n + 3) / 4, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
+    else
+      tb::k3_rows<L, false><<<dim3((p->n + 3) / 4, B), K::THREADS, smem_fft(), st>>>(dp, w, img, out_scale);
+    mark(4, 1);
+    TB_CUDA(cudaGetLastError());
+    return TB_OK;
+  }
+
+  static int ramp_rows(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,
+                       cudaStream_t st);
+};
+
+template <int NP>
+int launch_ramp(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
+  using K = tb::KShape<NP>;
+  tb::kr_ramp<NP><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int ramp_dispatch(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st);
+
+template <int L>
+int Launch<L>::ramp_rows(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,
+                         cudaStream_t st) {
+  return ramp_dispatch(p, in, out, total_rows, w, st);
+}
+
+// per-L entry points, defined in tb_inst.cu for each supported L
+#define TB_FOR_EACH_L(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+#define TB_DECLARE_L(N)                                                                                    \
+  int tb_configure_##N(tb_plan* p);                                                                      \
+  int tb_group_##N(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp,       \
+                   float scale, cudaStream_t st, cudaEvent_t* ev);                                       \
+  int tb_ramp_##N(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,           \
+                  cudaStream_t st);
+TB_FOR_EACH_L(TB_DECLARE_L)

@@ -351,13 +351,15 @@ def fbp(y: Sinogram, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
 
 
 def default_batch(plan: BstPlan) -> int:
-    """Slices per launch group: enough CTAs to fill 148 SMs for small slices,
-    one slice at a time for large ones (keeps intermediates L2-sized)."""
+    """Slices per launch group (two groups in flight on two streams): enough
+    CTAs to fill 148 SMs for small slices; 4 slices at L = 4096 (measured
+    best of 1/2/4/8 x lanes 1-4, profiles/README.md) keeps the K1 -> K2 -> K3
+    intermediates of the groups in flight near L2 size."""
     L = plan.radial_samples
     if L >= 4096:
-        return 2
-    if L >= 2048:
         return 4
+    if L >= 2048:
+        return 8
     return max(1, min(64, (4096 // L) ** 2))
 
 
