@@ -134,6 +134,12 @@ int tb_ss(const tb_plan* plan, const float* sino, float* image, int n_slices,
 int tb_fbp_ss(const tb_plan* plan, const float* sino, float* image, int n_slices,
               int batch, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Inspection of the K1 output: copies the polar half-spectrum of the last
+ * launch group run with `batch` on this workspace (first lane) into `dst`
+ * (device, [batch][rows][L/2] complex64 with rows = n_theta + 1 for
+ * half-turn input, 2 n_theta full turn), asynchronously on `stream`. */
+int tb_copy_polar(const tb_plan* plan, const void* workspace, int batch, void* dst, void* stream);
+
 /* Reset / read the non-finite flags kept in the workspace.  tb_read_status
  * synchronises `stream` and returns TB_OK, TB_ERR_NONFINITE_INPUT or
  * TB_ERR_NONFINITE_OUTPUT. */

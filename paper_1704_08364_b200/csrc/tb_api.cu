@@ -675,6 +675,17 @@ int tb_reset_status(const tb_plan* p, void* ws, void* stream) {
   return TB_OK;
 }
 
+int tb_copy_polar(const tb_plan* p, const void* ws, int batch, void* dst, void* stream) {
+  if (!p || !ws || !dst || batch < 1) return fail(TB_ERR_INVALID, "tb_copy_polar: bad argument");
+  int rc = set_device(p);
+  if (rc) return rc;
+  const Layout l = layout_for(p, batch);
+  const size_t bytes = (size_t)batch * p->dp.prow * p->H * sizeof(float2);
+  TB_CUDA(cudaMemcpyAsync(dst, static_cast<const char*>(ws) + l.polar, bytes, cudaMemcpyDeviceToDevice,
+                          static_cast<cudaStream_t>(stream)));
+  return TB_OK;
+}
+
 int tb_read_status(const tb_plan* p, const void* ws, void* stream) {
   if (!p || !ws) return fail(TB_ERR_INVALID, "null argument");
   int rc = set_device(p);

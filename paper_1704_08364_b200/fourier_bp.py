@@ -253,6 +253,15 @@ class NativePlan:
                              int(n_slices), ctypes.c_float(scale), self._stream(stream))
         _native.check(rc, "tb_ss")
 
+    def polar(self, workspace: torch.Tensor, batch: int, stream=None) -> torch.Tensor:
+        """K1 output of the last launch group (first lane) on this workspace:
+        [batch][rows][L/2] complex64 (tb_copy_polar)."""
+        rows = self.n_angles + 1 if not self.full_turn else self.n_angles
+        out = torch.empty((batch, rows, self.L // 2), dtype=torch.complex64, device=f"cuda:{self.device}")
+        _native.check(self._lib.tb_copy_polar(self._h, ctypes.c_void_p(workspace.data_ptr()), int(batch),
+                                              ctypes.c_void_p(out.data_ptr()), self._stream(stream)), "tb_copy_polar")
+        return out
+
     def reset_status(self, workspace: torch.Tensor, stream=None) -> None:
         _native.check(self._lib.tb_reset_status(self._h, ctypes.c_void_p(workspace.data_ptr()),
                                                 self._stream(stream)), "tb_reset_status")
