@@ -627,10 +627,14 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           // one 2x2 texel gather per component (TLD4, point sampling: exact
           // fp32 texels; the bilinear weights stay in fp32 below).  Texel
           // (u, v) = (r, t); clamp addressing reproduces min(r0 + 1, H - 1).
-          // Issued unconditionally (branch-free; outside nodes read r = 0).
           const float fx = (float)(ra + 1), fy = (float)(q * (p.n_theta + 1) + t0 + 1);
-          const float4 re = tex2Dgather<float4>(w.polar_tex, fx, fy, 0);
-          const float4 im = tex2Dgather<float4>(w.polar_tex, fx, fy, 1);
+          // nodes outside the disc (contiguous runs of b per column: whole
+          // warps) skip their gathers
+          float4 re = make_float4(0.f, 0.f, 0.f, 0.f), im = re;
+          if (in) {
+            re = tex2Dgather<float4>(w.polar_tex, fx, fy, 0);
+            im = tex2Dgather<float4>(w.polar_tex, fx, fy, 1);
+          }
           p00[j] = make_float2(re.w, im.w);  // (u0, v0) = (ra, t0)
           p01[j] = make_float2(re.z, im.z);  // (u1, v0) = (rb, t0)
           p10[j] = make_float2(re.x, im.x);  // (u0, v1) = (ra, t0 + 1)
