@@ -196,7 +196,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_1704_08364_b200 import fourier_bp as F
-    from paper_1704_08364_b200 import phantom
+    from paper_1704_08364_b200 import phantom, slabs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -211,16 +211,11 @@ def run_ours(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return slabs.max_over_ranks(x, device=dev)
 
     n = args.size
     plan = F.BstPlan(n, n)
-    slabs = F._split(n, world)
-    b, e = slabs[rank]
+    b, e = slabs.rank_slab(n, world, rank)
     S = e - b
     batch = args.batch or F.default_batch(plan)
 

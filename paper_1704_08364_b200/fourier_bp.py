@@ -374,13 +374,8 @@ def default_batch(plan: BstPlan) -> int:
 
 def _split(n: int, parts: int) -> list[tuple[int, int]]:
     """Contiguous [begin, end) slabs of n items over `parts` owners."""
-    base, extra = divmod(n, parts)
-    out, b = [], 0
-    for p in range(parts):
-        e = b + base + (1 if p < extra else 0)
-        out.append((b, e))
-        b = e
-    return out
+    from .slabs import split
+    return split(n, parts)
 
 
 def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan(), kernel: str = "bst",
