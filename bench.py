@@ -262,11 +262,22 @@ def run_ours(args):
     achieved = alg[dom] * slices_per_launch / (per_launch_ms / 1e3) / 1e9
     peak, peak_src = _peaks()
     traffic = None
+    issue = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
         if tr.get("size") == n and dom in tr.get("kernels", {}):
             traffic = tr["kernels"][dom]["dram_bytes_per_slice"] * slices_per_launch
+        # the path is bound by instruction issue, not HBM: every SM issues at
+        # most 4 warp instructions per clock, so the ncu-counted warp
+        # instructions per slice set a floor on the step time
+        if tr.get("size") == n:
+            wi = sum(k.get("warp_inst_per_slice", 0.0) for k in tr["kernels"].values()) * S
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            mhz = (clk or {}).get("sm_mhz") or 1965.0
+            floor_ms = wi / (sms * 4 * mhz * 1e6) * 1e3
+            issue = {"bound": "issue", "warp_inst_per_step": wi, "floor_ms": floor_ms,
+                     "frac": floor_ms / ms_step, "source": tr.get("source")}
     except Exception:
         pass
     nat.read_status(ws)
@@ -316,6 +327,7 @@ def run_ours(args):
             "path_roofline": {"algorithmic_bytes_per_volume": alg["total"] * n,
                               "achieved_gbs": alg["total"] * n / (ms_step / 1e3) / 1e9 / world,
                               "frac_per_gpu": alg["total"] * n / (ms_step / 1e3) / 1e9 / world / peak},
+            "issue_roofline": issue,
             "stage_ms_per_step": {k: v for k, v in stage.items() if v > 0},
             "gpu_launches": sum(launches.values()) * args.steps,
             "e2e": e2e,
