@@ -55,6 +55,8 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-slices", type=int, default=None)
+    ap.add_argument("--no-ss", action="store_true", help="skip the slant-stack comparator sample")
+    ap.add_argument("--ss-slices", type=int, default=8)
     return ap.parse_args()
 
 
@@ -282,6 +284,25 @@ def run_ours(args):
         pass
     nat.read_status(ws)
 
+    # BASELINE configs[4]: the brute-force O(N^3) slant-stack backprojection
+    # (fbp kernel "ss", projector.py:126-158) on the same inputs, timed on a
+    # bounded sample of this rank's slices (device-resident, CUDA events)
+    ss = None
+    if not args.no_ss and S > 0:
+        k = min(S, args.ss_slices)
+        nat.run("fbp_ss", sino, img, k, batch, ws, stream)  # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nat.run("fbp_ss", sino, img, k, batch, ws, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ss_ms = e0.elapsed_time(e1) / k
+        ss = {"kernel": "k5_slant (fbp kernel='ss')", "slices_sampled": k, "ms_per_slice": ss_ms,
+              "voxels_per_s": n * n / (ss_ms / 1e3), "bst_ms_per_slice": ms_step / S,
+              "bst_speedup": ss_ms / (ms_step / S)}
+        nat.read_status(ws)
+
     # end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -330,6 +351,7 @@ def run_ours(args):
             "issue_roofline": issue,
             "stage_ms_per_step": {k: v for k, v in stage.items() if v > 0},
             "gpu_launches": sum(launches.values()) * args.steps,
+            "ss_comparator": ss,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk,
