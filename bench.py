@@ -56,6 +56,7 @@ def _args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-slices", type=int, default=None)
     ap.add_argument("--no-ss", action="store_true", help="skip the slant-stack comparator sample")
+    ap.add_argument("--no-counts", action="store_true", help="skip the fused-normalisation counts step")
     ap.add_argument("--ss-slices", type=int, default=8)
     return ap.parse_args()
 
@@ -284,6 +285,26 @@ def run_ours(args):
         pass
     nat.read_status(ws)
 
+    # the same volume as raw transmission counts with the reference pipeline's
+    # normalize stage fused into K1 (tb_fbp_counts; flat 2, dark 0 frames)
+    counts_path = None
+    if not args.no_counts:
+        flat = torch.full((n, n), 2.0, device=dev)
+        dark = torch.zeros((n, n), device=dev)
+        nat.run_counts(sino, flat, dark, 1e-6, img, S, batch, ws, stream)  # warm-up
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        nat.run_counts(sino, flat, dark, 1e-6, img, S, batch, ws, stream)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cms = max_over_ranks(c0.elapsed_time(c1))
+        counts_path = {"what": "fbp of transmission counts, normalize fused into K1 (tb_fbp_counts)",
+                       "ms_per_step": cms, "voxels_per_s": (n ** 3) / (cms / 1e3),
+                       "overhead_vs_line_integrals": cms / ms_step - 1.0}
+        nat.read_status(ws)
+        del flat, dark
+
     # BASELINE configs[4]: the brute-force O(N^3) slant-stack backprojection
     # (fbp kernel "ss", projector.py:126-158) on the same inputs, timed on a
     # bounded sample of this rank's slices (device-resident, CUDA events)
@@ -352,6 +373,7 @@ def run_ours(args):
             "stage_ms_per_step": {k: v for k, v in stage.items() if v > 0},
             "gpu_launches": sum(launches.values()) * args.steps,
             "ss_comparator": ss,
+            "counts_path": counts_path,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk,

@@ -11,6 +11,8 @@
  *   tb_ramp                           <- ramp_filter               fourier_bp.py:490-505
  *   tb_ss         (kernel "ss")       <- backproject_ss            projector.py:126-158
  *   tb_fbp_ss                         <- fbp(kernel="ss")          fourier_bp.py:525-527
+ *   tb_normalize                      <- preprocess.normalize      preprocess.py:59-74
+ *   tb_fbp_counts                     <- normalize + fbp stages    pipeline.py:447-459, 486-518
  *
  * Conventions (grids.py): sinograms are angle-major float32 [B][A][n_t]
  * (A = n_theta, or 2*n_theta for full-turn input); images are float32
@@ -116,6 +118,19 @@ int tb_fbp(const tb_plan* plan, const float* sino, float* image, int n_slices,
 int tb_fbp_profiled(const tb_plan* plan, const float* sino, float* image, int n_slices,
                     int batch, void* workspace, size_t workspace_bytes, void* stream,
                     double* stage_ms);
+
+/* fbp on transmission counts: the normalisation prologue
+ * y = -ln(max(I - D, eps) / max(I0 - D, eps))   (preprocess.py:59-74,
+ * pipeline.py:447-459) fused into the radial kernel's load, then as tb_fbp.
+ * flat (I0) and dark (D) are device frames [A][n_t] shared by every slice. */
+int tb_fbp_counts(const tb_plan* plan, const float* counts, const float* flat, const float* dark,
+                  double eps, float* image, int n_slices, int batch, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* normalize alone (preprocess.normalize, preprocess.py:59-74): counts
+ * [B][A][n_t] -> line integrals, same shape.  NaN counts stay NaN. */
+int tb_normalize(const tb_plan* plan, const float* counts, const float* flat, const float* dark,
+                 double eps, float* out, int n_slices, void* stream);
 
 /* BST backprojection only (input already ramp-filtered; no 1/(2 pi)). */
 int tb_bst(const tb_plan* plan, const float* sino, float* image, int n_slices,

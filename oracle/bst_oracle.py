@@ -221,6 +221,17 @@ class OraclePlan:
 # ---------------------------------------------------------------------------
 
 
+def normalize(counts: np.ndarray, flat: np.ndarray, dark: np.ndarray, eps: float = 1e-6) -> np.ndarray:
+    """Transmission counts to line integrals, -log(max(I - D, eps) / max(I0 - D, eps))
+    (preprocess.py:59-74; np.maximum propagates NaN like the reference)."""
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    counts = np.asarray(counts, dtype=np.float64)
+    num = np.maximum(counts - np.asarray(dark, dtype=np.float64), eps)
+    den = np.maximum(np.asarray(flat, dtype=np.float64) - np.asarray(dark, dtype=np.float64), eps)
+    return -np.log(num / den)
+
+
 def ramp_filter(y: np.ndarray, plan: OraclePlan) -> np.ndarray:
     """Rows of ``y`` through the padded 2*pi*|f| ramp (fourier_bp.py:469-505)."""
     y = np.asarray(y, dtype=np.float64)

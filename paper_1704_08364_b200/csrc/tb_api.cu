@@ -64,8 +64,8 @@ int lanes_cfg() {
 }
 
 struct Layout {
-  size_t polar, rowcoef, part, common, common2, coefmean, columns, filtered, status, total;
-  size_t lane_bytes;  // stride between the per-lane regions (all but status)
+  size_t polar, rowcoef, part, common, common2, coefmean, columns, filtered, status, normtab, total;
+  size_t lane_bytes;  // stride between the per-lane regions (all but status / normtab)
 };
 
 Layout layout_for(const tb_plan* p, int B) {
@@ -77,6 +77,7 @@ Layout layout_for(const tb_plan* p, int B) {
     return o;
   };
   l.status = take(2 * sizeof(int));  // first: its offset does not depend on the batch
+  l.normtab = take((size_t)p->rows * p->n_t * sizeof(float2));  // count-input frames table
   l.polar = take((size_t)B * p->dp.prow * p->H * sizeof(float2));
   l.rowcoef = take((size_t)B * p->rows * sizeof(float));
   l.part = take((size_t)B * p->groups * std::max(p->S, 1) * sizeof(float));
@@ -105,6 +106,8 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   w.columns = reinterpret_cast<float2*>(base + l.columns);
   w.filtered = reinterpret_cast<float*>(base + l.filtered);
   w.status = reinterpret_cast<int*>(static_cast<char*>(ws) + l.status);
+  w.normtab = nullptr;
+  w.norm_eps = 0.f;
   w.groups = p->groups;
   w.pairs_per_cta = p->pairs_per_cta;
   w.polar_tex = polar_texture(p, w.polar, B * p->dp.prow);
@@ -197,12 +200,27 @@ int set_device(const tb_plan* p) {
   return TB_OK;
 }
 
+// transmission-count input (tb_fbp_counts): flat / dark frames [rows][n_t]
+struct NormFrames {
+  const float* flat;
+  const float* dark;
+  double eps;
+};
+
 int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, int batch, void* ws,
-                 size_t ws_bytes, void* stream, bool ramp, float scale, double* stage_ms = nullptr) {
+                 size_t ws_bytes, void* stream, bool ramp, float scale, double* stage_ms = nullptr,
+                 const NormFrames* norm = nullptr) {
   int rc = check_exec_args(p, sino, img, n_slices, batch, ws, ws_bytes);
   if (rc) return rc;
   if ((rc = set_device(p))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float2* normtab = nullptr;
+  if (norm) {  // (D, 1 / max(I0 - D, eps)) once per call, read by every slice's K1
+    normtab = reinterpret_cast<float2*>(static_cast<char*>(ws) + layout_for(p, batch).normtab);
+    const int cnt = p->rows * p->n_t;
+    tb::k_norm_table<<<(cnt + 255) / 256, 256, 0, st>>>(norm->flat, norm->dark, (float)norm->eps, normtab, cnt);
+    TB_CUDA(cudaGetLastError());
+  }
   const size_t in_stride = (size_t)p->rows * p->n_t;
   const size_t out_stride = (size_t)p->n * p->n;
   const int ngroups = (n_slices + batch - 1) / batch;
@@ -234,6 +252,10 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
     const int B = std::min(batch, n_slices - s0);
     const int lane = g % lanes;
     Work w = work_for(p, batch, ws, lane);
+    if (norm) {
+      w.normtab = normtab;
+      w.norm_eps = (float)norm->eps;
+    }
     cudaStream_t ls = lane ? aux[lane] : st;
     rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, ls,
                       stage_ms ? evs.data() + (size_t)g * 10 : nullptr);
@@ -604,6 +626,33 @@ int tb_fbp_profiled(const tb_plan* p, const float* sino, float* image, int n_sli
   if (!stage_ms) return fail(TB_ERR_INVALID, "null stage_ms");
   return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)),
                       stage_ms);
+}
+
+int tb_fbp_counts(const tb_plan* p, const float* counts, const float* flat, const float* dark, double eps,
+                  float* image, int n_slices, int batch, void* ws, size_t ws_bytes, void* stream) {
+  if (!(eps > 0.0)) return fail(TB_ERR_INVALID, "eps must be positive");
+  if (n_slices > 0 && (!flat || !dark)) return fail(TB_ERR_INVALID, "null flat/dark frame");
+  const NormFrames nf{flat, dark, eps};
+  return run_bst_like(p, counts, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)),
+                      nullptr, &nf);
+}
+
+int tb_normalize(const tb_plan* p, const float* counts, const float* flat, const float* dark, double eps, float* out,
+                 int n_slices, void* stream) {
+  if (!p) return fail(TB_ERR_INVALID, "null plan");
+  if (!(eps > 0.0)) return fail(TB_ERR_INVALID, "eps must be positive");
+  if (n_slices < 0) return fail(TB_ERR_INVALID, "n_slices must be >= 0");
+  if (n_slices == 0) return TB_OK;
+  if (!counts || !flat || !dark || !out) return fail(TB_ERR_INVALID, "null data pointer");
+  int rc = set_device(p);
+  if (rc) return rc;
+  const int frame = p->rows * p->n_t;
+  const long long total = (long long)n_slices * frame;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  tb::k_normalize<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(counts, flat, dark, (float)eps, out, total,
+                                                                         frame);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
 }
 
 int tb_bst(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws, size_t ws_bytes,

@@ -60,6 +60,10 @@ struct Work {
   float2* columns;
   float* filtered;
   int* status;  // [0] non-finite input, [1] non-finite output
+  // transmission-count input (NORM kernels): per input row and detector
+  // (dark D, 1 / max(I0 - D, eps)) and eps
+  const float2* normtab;
+  float norm_eps;
   int groups;   // K1 CTAs per slice (partial-sum groups)
   int pairs_per_cta;
   // texture view of this lane's polar region (pitch 2D, float2 texels,
@@ -84,9 +88,20 @@ struct KShape {
 };
 
 // ---------------------------------------------------------------------------
-// K1: radial kernel (fused ramp when npad == L)
+// Normalisation prologue (preprocess.py:59-74): transmission counts to line
+// integrals, y = -ln(max(I - D, eps) / max(I0 - D, eps)).  nt = (D, 1 /
+// max(I0 - D, eps)) per input row and detector (k_norm_table).  A NaN
+// difference stays NaN (np.maximum propagates it; fmaxf would not).
 // ---------------------------------------------------------------------------
-template <int L, bool RAMP>
+__device__ __forceinline__ float norm_line(float I, float2 nt, float eps) {
+  const float num = I - nt.x;
+  return -__logf((num != num ? num : fmaxf(num, eps)) * nt.y);
+}
+
+// ---------------------------------------------------------------------------
+// K1: radial kernel (fused ramp when npad == L; fused normalisation when NORM)
+// ---------------------------------------------------------------------------
+template <int L, bool RAMP, bool NORM>
 __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
@@ -147,6 +162,11 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
           a = r0[idx];
           if (has1) b = r1[idx];
           bad |= !isfinite(a) || !isfinite(b);
+          if constexpr (NORM) {
+            const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
+            a = norm_line(a, __ldg(nt), w.norm_eps);
+            if (has1) b = norm_line(b, __ldg(nt + p.n_t), w.norm_eps);
+          }
         }
         v[i] = make_float2(a, b);
       }
@@ -163,6 +183,11 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
           a = __ldg(y0 + idx);
           if (has1) b = __ldg(y1 + idx);
           bad |= !isfinite(a) || !isfinite(b);
+          if constexpr (NORM) {
+            const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
+            a = norm_line(a, __ldg(nt), w.norm_eps);
+            if (has1) b = norm_line(b, __ldg(nt + p.n_t), w.norm_eps);
+          }
         }
         v[i] = make_float2(a, b);
       }
@@ -244,7 +269,7 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
 // ---------------------------------------------------------------------------
 // KR: standalone ramp filter (rows -> rows), fourier_bp.py:469-505
 // ---------------------------------------------------------------------------
-template <int NP>
+template <int NP, bool NORM>
 __global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const float* __restrict__ sino,
                                                                float* __restrict__ out, int total_rows, Work w) {
   using K = KShape<NP>;
@@ -266,6 +291,12 @@ __global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const 
       a = __ldg(y0 + idx);
       if (has1) b = __ldg(y1 + idx);
       bad |= !isfinite(a) || !isfinite(b);
+      if constexpr (NORM) {
+        // input row j0 of slice (j0 / rows) -> frame row j0 % rows
+        const float2* nt = w.normtab + (size_t)(j0 % p.rows) * p.n_t + idx;
+        a = norm_line(a, __ldg(nt), w.norm_eps);
+        if (has1) b = norm_line(b, __ldg(w.normtab + (size_t)(j1 % p.rows) * p.n_t + idx), w.norm_eps);
+      }
     }
     v[i] = make_float2(a, b);
   }
@@ -859,6 +890,29 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k3_rows(D
 // K5: slant-stack backprojection (projector.py:126-158)
 // ---------------------------------------------------------------------------
 #ifdef TB_API_KERNELS
+// (D, 1 / max(I0 - D, eps)) per input row and detector
+__global__ void __launch_bounds__(256) k_norm_table(const float* __restrict__ flat, const float* __restrict__ dark,
+                                                    float eps, float2* __restrict__ tab, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const float d = dark[i];
+  const float den = flat[i] - d;
+  tab[i] = make_float2(d, 1.f / (den != den ? den : fmaxf(den, eps)));
+}
+
+// standalone normalize over n slices of [rows][n_t] counts
+__global__ void __launch_bounds__(256) k_normalize(const float* __restrict__ counts, const float* __restrict__ flat,
+                                                   const float* __restrict__ dark, float eps, float* __restrict__ out,
+                                                   long long total, int frame) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(i % frame);
+    const float d = __ldg(dark + f);
+    const float den = __ldg(flat + f) - d;
+    out[i] = norm_line(counts[i], make_float2(d, 1.f / (den != den ? den : fmaxf(den, eps))), eps);
+  }
+}
+
 __global__ void __launch_bounds__(256) k5_slant(DevPlan p, const float* __restrict__ rows, int n_ang,
                                                 float* __restrict__ img, float scale, Work w) {
   const int m1 = blockIdx.x * 16 + (threadIdx.x & 15);

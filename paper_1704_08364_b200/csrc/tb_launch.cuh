@@ -79,8 +79,9 @@ struct Launch {
   }
 
   static int configure(tb_plan* p) {
-    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
     TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
@@ -88,7 +89,8 @@ struct Launch {
       TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
       TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     }
-    TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     return TB_OK;
   }
 
@@ -116,10 +118,12 @@ struct Launch {
     }
     dim3 g1(p->groups, B);
     mark(1, 0);
-    if (fused)
-      tb::k1_radial<L, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    if (fused && w.normtab)  // transmission counts: normalisation fused into the load
+      tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    else if (fused)
+      tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
     else
-      tb::k1_radial<L, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+      tb::k1_radial<L, false, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
     mark(1, 1);
     mark(2, 0);
     tb::k1b_common<L><<<B, K::K1B_THREADS, smem_k1b(p), st>>>(dp, w);
@@ -150,7 +154,10 @@ struct Launch {
 template <int NP>
 int launch_ramp(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
   using K = tb::KShape<NP>;
-  tb::kr_ramp<NP><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);
+  if (w.normtab)  // unfused ramp on transmission counts: normalisation in its load
+    tb::kr_ramp<NP, true><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);
+  else
+    tb::kr_ramp<NP, false><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }

@@ -232,6 +232,24 @@ class NativePlan:
                 self._stream(stream))
         _native.check(rc, f"tb_{op}")
 
+    def run_counts(self, counts: torch.Tensor, flat: torch.Tensor, dark: torch.Tensor, eps: float,
+                   image: torch.Tensor, n_slices: int, batch: int, workspace: torch.Tensor, stream=None) -> None:
+        """fbp of transmission counts with the normalisation fused into K1
+        (tb_fbp_counts); flat / dark are device frames [A][n_t] f32."""
+        rc = self._lib.tb_fbp_counts(self._h, ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(flat.data_ptr()),
+                                     ctypes.c_void_p(dark.data_ptr()), ctypes.c_double(eps),
+                                     ctypes.c_void_p(image.data_ptr()), int(n_slices), int(batch),
+                                     ctypes.c_void_p(workspace.data_ptr()), ctypes.c_size_t(workspace.numel()),
+                                     self._stream(stream))
+        _native.check(rc, "tb_fbp_counts")
+
+    def normalize(self, counts: torch.Tensor, flat: torch.Tensor, dark: torch.Tensor, eps: float,
+                  out: torch.Tensor, n_slices: int, stream=None) -> None:
+        rc = self._lib.tb_normalize(self._h, ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(flat.data_ptr()),
+                                    ctypes.c_void_p(dark.data_ptr()), ctypes.c_double(eps),
+                                    ctypes.c_void_p(out.data_ptr()), int(n_slices), self._stream(stream))
+        _native.check(rc, "tb_normalize")
+
     def run_profiled(self, sino: torch.Tensor, image: torch.Tensor, n_slices: int, batch: int,
                      workspace: torch.Tensor, stream=None) -> dict:
         """tb_fbp with per-stage CUDA events; returns summed device ms per stage."""
@@ -378,9 +396,22 @@ def _split(n: int, parts: int) -> list[tuple[int, int]]:
     return split(n, parts)
 
 
+def _frames_on(frames, dev: int, A: int, n_t: int):
+    """(flat, dark) of a FlatDarkFrames as float32 [A][n_t] tensors on cuda:dev."""
+    out = []
+    for x in (frames.flat, frames.dark):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float32))
+        t = t.to(device=f"cuda:{dev}", dtype=torch.float32).contiguous()
+        if tuple(t.shape) != (A, n_t):
+            raise ValueError(f"counts shape {(A, n_t)} does not match frames {tuple(t.shape)}")
+        out.append(t)
+    return out
+
+
 def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan(), kernel: str = "bst",
                full_turn: bool = False, out: torch.Tensor | None = None, batch: int | None = None,
-               devices=None, chunk: int | None = None, check: bool = True) -> torch.Tensor:
+               devices=None, chunk: int | None = None, check: bool = True, frames=None,
+               eps: float = 1e-6) -> torch.Tensor:
     """Reconstruct a sinogram volume [S][A][n_t] -> image volume [S][n][n].
 
     * CUDA tensor input: computed on that device, asynchronously on the
@@ -393,7 +424,16 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     ``kernel`` is "bst" (fbp) or "ss" (ramp + slant stack); with
     ``kernel="none"`` the input is taken as already filtered
     (bst_backproject semantics, no 1/(2 pi)).
+
+    With ``frames`` (a ``preprocess.FlatDarkFrames`` of [A][n_t] flat and
+    dark fields) the input is raw transmission counts: the reference
+    pipeline's normalize stage, -ln(max(I - D, eps) / max(I0 - D, eps))
+    (preprocess.py:59-74, pipeline.py:447-459), runs fused into the radial
+    kernel's load for kernel "bst" (device or host input), or as a separate
+    pass before "ss" / "none" (device input).
     """
+    if frames is not None and not eps > 0:
+        raise ValueError("eps must be positive")
     if kernel not in ("bst", "ss", "none"):
         raise ValueError(f"unknown kernel {kernel!r}")
     if isinstance(sino, np.ndarray):
@@ -419,15 +459,25 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
         ws = nat.new_workspace(min(batch, max(S, 1)))
         with torch.cuda.device(dev):
             nat.reset_status(ws)
-            if S:
+            if S and frames is not None:
+                flat, dark = _frames_on(frames, dev, A, n_t)
+                if op == "fbp":
+                    nat.run_counts(sino, flat, dark, eps, out, S, min(batch, S), ws)
+                else:
+                    line = torch.empty_like(sino)
+                    nat.normalize(sino, flat, dark, eps, line, S)
+                    nat.run(op, line, out, S, min(batch, S), ws)
+            elif S:
                 nat.run(op, sino, out, S, min(batch, S), ws)
             if check:
                 nat.read_status(ws)
         return out
-    return _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check)
+    if frames is not None and op != "fbp":
+        raise ValueError("host-resident counts are supported for kernel 'bst' (fused normalisation)")
+    return _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check, frames, eps)
 
 
-def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check):
+def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check, frames=None, eps=1e-6):
     S, A, n_t = sino.shape
     n = plan.output_n
     if devices is None:
@@ -459,6 +509,7 @@ def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, c
                 "cmp": [torch.cuda.Event() for _ in range(2)],
                 "d2h": [torch.cuda.Event() for _ in range(2)],
                 "k": 0, "chunk": m,
+                "frames": _frames_on(frames, dev, A, n_t) if frames is not None else None,
             }
             nat.reset_status(st["ws"], st["s_cmp"])
         states.append(st)
@@ -480,7 +531,11 @@ def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, c
                     st["h2d"][k].record(st["s_in"])
                 st["s_cmp"].wait_event(st["h2d"][k])
                 st["s_cmp"].wait_event(st["d2h"][k])  # output buffer k free
-                st["nat"].run(op, st["inb"][k], st["outb"][k], m, min(batch, st["chunk"]), st["ws"], st["s_cmp"])
+                if st["frames"] is not None:
+                    st["nat"].run_counts(st["inb"][k], *st["frames"], eps, st["outb"][k], m, min(batch, st["chunk"]),
+                                         st["ws"], st["s_cmp"])
+                else:
+                    st["nat"].run(op, st["inb"][k], st["outb"][k], m, min(batch, st["chunk"]), st["ws"], st["s_cmp"])
                 st["cmp"][k].record(st["s_cmp"])
                 with torch.cuda.stream(st["s_out"]):
                     st["s_out"].wait_event(st["cmp"][k])

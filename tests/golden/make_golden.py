@@ -51,6 +51,30 @@ def _case(name, sino, plan_kw, filt_kw=None, full_turn=False, ss=False):
     print(f"{name}: sino {sino.shape} -> {out['fbp_bst'].shape}")
 
 
+def _norm_case(name, y, i0, dark_level, rng, plan_kw=None):
+    """Counts -> normalize -> fbp through the reference (preprocess.py:59-74,
+    fourier_bp.py:508-530); frames vary per angle and detector, and a few
+    samples fall below the dark level (the eps clamp)."""
+    from tomoblocks import preprocess as ref_pre
+    plan_kw = plan_kw or {}
+    v, n_t = y.shape
+    flat = (i0 * (1.0 + 0.02 * rng.standard_normal((v, n_t)))).astype(np.float32)
+    dark = (dark_level * (1.0 + 0.1 * rng.random((v, n_t)))).astype(np.float32)
+    counts = (flat - dark) * np.exp(-y) * (1.0 + 0.01 * rng.standard_normal((v, n_t))) + dark
+    counts = counts.astype(np.float32)
+    counts[3, 5] = dark[3, 5] - 1.0  # below dark: clamped at eps
+    frames = ref_pre.FlatDarkFrames(flat=flat.astype(np.float64), dark=dark.astype(np.float64))
+    line = ref_pre.normalize(counts.astype(np.float64), frames)
+    ys = Sinogram(DetectorAxis(n_t), AngleAxis(v), line)
+    plan = ref_fbp.BstPlan(n_t=n_t, n_theta=v, **plan_kw)
+    out = {"counts": counts, "flat": flat, "dark": dark, "eps": np.float64(1e-6), "normalize": line,
+           "fbp_bst": ref_fbp.fbp(ys, plan, ref_fbp.FilterPlan(), kernel="bst").data,
+           "params": np.array(json.dumps({"plan": plan_kw}))}
+    os.makedirs(os.path.join(HERE, "norm"), exist_ok=True)
+    np.savez_compressed(os.path.join(HERE, "norm", f"{name}.npz"), **out)
+    print(f"{name}: counts {counts.shape} -> {out['fbp_bst'].shape}")
+
+
 def main():
     rng0 = np.random.default_rng(0)
     rng1 = np.random.default_rng(1)
@@ -80,6 +104,11 @@ def main():
     _case("fullturn128", ft + rng0.normal(0.0, 0.02, ft.shape), {}, full_turn=True, ss=True)
     # tiny detector
     _case("tiny16x12", rng1.normal(0.0, 1.0, (12, 16)), {}, ss=True)
+    # transmission counts through the normalisation prologue
+    rng2 = np.random.default_rng(2)
+    _norm_case("norm_shepp128", ellipse_sinogram(SHEPP_LOGAN, 128, 128) * 0.5, 1.0e4, 100.0, rng2)
+    _norm_case("norm_ellipse256x192", ellipse_sinogram([(1.0, 0.5, 0.4, 0.1, -0.05, 0.0)], 256, 192),
+               4.0e3, 50.0, rng2, {"output_n": 200})
     import scipy
     with open(os.path.join(HERE, "versions.json"), "w") as f:
         json.dump({"numpy": np.__version__, "scipy": scipy.__version__,
