@@ -11,6 +11,7 @@
  *   tb_ramp                           <- ramp_filter               fourier_bp.py:490-505
  *   tb_ss         (kernel "ss")       <- backproject_ss            projector.py:126-158
  *   tb_fbp_ss                         <- fbp(kernel="ss")          fourier_bp.py:525-527
+ *   tb_forward                        <- forward_project           projector.py:94-123
  *   tb_normalize                      <- preprocess.normalize      preprocess.py:59-74
  *   tb_fbp_counts                     <- normalize + fbp stages    pipeline.py:447-459, 486-518
  *
@@ -144,6 +145,13 @@ int tb_ramp(const tb_plan* plan, const float* sino, float* out, int n_slices,
  * grid, multiplied by `scale` (1 for backproject_ss). */
 int tb_ss(const tb_plan* plan, const float* sino, float* image, int n_slices,
           float scale, void* stream);
+
+/* Forward projector (projector.forward_project, projector.py:94-123): line
+ * integrals of images [B][n][n] (n = plan output_n) on the plan's (t, theta)
+ * grid -> sinograms [B][A][n_t]; step_length in (0, 1] pixel sizes, interp
+ * tb_interp.  The adjoint partner of tb_ss. */
+int tb_forward(const tb_plan* plan, const float* image, float* sino, int n_slices,
+               double step_length, int interp, void* stream);
 
 /* fbp(kernel="ss"): ramp -> slant stack -> x 1/(2 pi). */
 int tb_fbp_ss(const tb_plan* plan, const float* sino, float* image, int n_slices,

@@ -221,6 +221,49 @@ class OraclePlan:
 # ---------------------------------------------------------------------------
 
 
+def _sample_image(img: np.ndarray, u1, u2, nearest: bool) -> np.ndarray:
+    """Image samples at points, pixel-centre convention, zero outside
+    (projector.py:65-91)."""
+    n = img.shape[0]
+    du = 2.0 / n
+    fx = (u1 + 1.0) / du - 0.5
+    fy = (u2 + 1.0) / du - 0.5
+    if nearest:
+        ix, iy = np.rint(fx).astype(np.int64), np.rint(fy).astype(np.int64)
+        ok = (ix >= 0) & (ix < n) & (iy >= 0) & (iy < n)
+        return np.where(ok, img[np.clip(iy, 0, n - 1), np.clip(ix, 0, n - 1)], 0.0)
+    x0, y0 = np.floor(fx).astype(np.int64), np.floor(fy).astype(np.int64)
+    wx, wy = fx - x0, fy - y0
+    out = np.zeros(np.broadcast(fx, fy).shape)
+    for dy in (0, 1):
+        for dx in (0, 1):
+            ix, iy = x0 + dx, y0 + dy
+            w = (wx if dx else 1.0 - wx) * (wy if dy else 1.0 - wy)
+            ok = (ix >= 0) & (ix < n) & (iy >= 0) & (iy < n)
+            out += np.where(ok, img[np.clip(iy, 0, n - 1), np.clip(ix, 0, n - 1)] * w, 0.0)
+    return out
+
+
+def forward_project(img: np.ndarray, n_t: int, n_angles: int, full_turn: bool = False,
+                    step_length: float = 0.5, nearest: bool = False) -> np.ndarray:
+    """Midpoint-rule line integrals along every (theta_j, t_i) ray over the
+    circumscribed diameter (projector.py:94-123); [n_angles][n_t]."""
+    n = img.shape[0]
+    h = step_length * (2.0 / n)
+    half = np.sqrt(2.0)
+    m = int(np.ceil(2.0 * half / h))
+    ell = -half + (np.arange(m) + 0.5) * h
+    t = -1.0 + 2.0 * np.arange(n_t) / (n_t - 1)
+    th = (2.0 * np.pi if full_turn else np.pi) / n_angles * np.arange(n_angles)
+    out = np.empty((n_angles, n_t))
+    for j in range(n_angles):
+        c, s = np.cos(th[j]), np.sin(th[j])
+        u1 = t[:, None] * c - ell[None, :] * s
+        u2 = t[:, None] * s + ell[None, :] * c
+        out[j] = _sample_image(img, u1, u2, nearest).sum(axis=1) * h
+    return out
+
+
 def normalize(counts: np.ndarray, flat: np.ndarray, dark: np.ndarray, eps: float = 1e-6) -> np.ndarray:
     """Transmission counts to line integrals, -log(max(I - D, eps) / max(I0 - D, eps))
     (preprocess.py:59-74; np.maximum propagates NaN like the reference)."""

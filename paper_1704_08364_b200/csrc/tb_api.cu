@@ -694,6 +694,31 @@ int tb_ss(const tb_plan* p, const float* sino, float* image, int n_slices, float
   return TB_OK;
 }
 
+int tb_forward(const tb_plan* p, const float* image, float* sino, int n_slices, double step_length, int interp,
+               void* stream) {
+  if (!p) return fail(TB_ERR_INVALID, "null plan");
+  if (!(step_length > 0.0 && step_length <= 1.0))
+    return fail(TB_ERR_INVALID, "step_length must be in (0, 1], got " + std::to_string(step_length));
+  if (interp != TB_INTERP_BILINEAR && interp != TB_INTERP_NEAREST) return fail(TB_ERR_INVALID, "unknown interpolation");
+  if (n_slices < 0) return fail(TB_ERR_INVALID, "n_slices must be >= 0");
+  if (n_slices == 0) return TB_OK;
+  if (!image || !sino) return fail(TB_ERR_INVALID, "null data pointer");
+  int rc = set_device(p);
+  if (rc) return rc;
+  // projector.py:106-110: h = step x pixel size, m = ceil(2 sqrt2 / h)
+  const double h = step_length * (2.0 / p->n);
+  const int m = (int)std::ceil(2.0 * std::sqrt(2.0) / h);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int s = 0; s < n_slices; s += 65535) {
+    const int B = std::min(65535, n_slices - s);
+    dim3 grid((p->n_t + 127) / 128, p->rows, B);
+    tb::k6_forward<<<grid, 128, 0, st>>>(p->dp, image + (size_t)s * p->n * p->n, sino + (size_t)s * p->rows * p->n_t,
+                                          p->rows, h, m, interp == TB_INTERP_NEAREST ? 1 : 0);
+  }
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
 int tb_fbp_ss(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws,
               size_t ws_bytes, void* stream) {
   int rc = check_exec_args(p, sino, image, n_slices, batch, ws, ws_bytes);

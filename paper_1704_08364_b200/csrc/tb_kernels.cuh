@@ -913,6 +913,79 @@ __global__ void __launch_bounds__(256) k_normalize(const float* __restrict__ cou
   }
 }
 
+// ---------------------------------------------------------------------------
+// K6: forward projector (projector.py:94-123): line integral of an n x n
+// image (pixel-centre convention, zero outside) along each (theta_j, t_i)
+// ray, midpoint rule with step h over the circumscribed diameter, samples
+// bilinear (or nearest, np.rint half-even) in the image.  One thread per
+// (slice, angle, detector); coordinates and the sum in fp64 like the
+// reference; the sample loop is clipped to the ray's intersection with the
+// one-pixel-padded image square (samples outside contribute exactly 0).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k6_forward(DevPlan p, const float* __restrict__ img, float* __restrict__ sino,
+                                                  int n_ang, double h, int m, int nearest) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int q = blockIdx.z;
+  if (i >= p.n_t) return;
+  const int n = p.n;
+  const double2 cs = __ldg(p.ss_cs + j);
+  const double t = -1.0 + 2.0 * (double)i / (double)(p.n_t - 1);
+  const double du = 2.0 / n, inv_du = 0.5 * n;
+  const double half = 1.4142135623730951;  // sqrt(2)
+  const float* im = img + (size_t)q * n * n;
+  // ray point at ell: u = t (c, s) + ell (-s, c); keep |u1|, |u2| <= 1 + 1.5 du
+  double lo = -half, hi = half;
+  const double lim = 1.0 + 1.5 * du;
+  auto clip = [&](double base, double dir) {
+    if (fabs(dir) < 1e-300) {
+      if (fabs(base) > lim) { lo = 1.0; hi = -1.0; }
+      return;
+    }
+    double a = (-lim - base) / dir, b = (lim - base) / dir;
+    if (a > b) { const double x = a; a = b; b = x; }
+    lo = fmax(lo, a);
+    hi = fmin(hi, b);
+  };
+  clip(t * cs.x, -cs.y);
+  clip(t * cs.y, cs.x);
+  double acc = 0.0;
+  if (hi >= lo) {
+    // samples ell_k = -sqrt2 + (k + 1/2) h inside [lo, hi] (one extra each side)
+    const int k0 = max(0, (int)floor((lo + half) / h - 0.5) - 1);
+    const int k1 = min(m - 1, (int)ceil((hi + half) / h - 0.5) + 1);
+    for (int k = k0; k <= k1; ++k) {
+      const double ell = -half + ((double)k + 0.5) * h;
+      const double u1 = t * cs.x - ell * cs.y;
+      const double u2 = t * cs.y + ell * cs.x;
+      const double fx = (u1 + 1.0) * inv_du - 0.5;
+      const double fy = (u2 + 1.0) * inv_du - 0.5;
+      if (nearest) {
+        const int ix = (int)rint(fx), iy = (int)rint(fy);
+        if (ix >= 0 && ix < n && iy >= 0 && iy < n) acc += (double)__ldg(im + (size_t)iy * n + ix);
+      } else {
+        const double x0f = floor(fx), y0f = floor(fy);
+        const int x0 = (int)x0f, y0 = (int)y0f;
+        const double wx = fx - x0f, wy = fy - y0f;
+        const bool xa = x0 >= 0 && x0 < n, xb = x0 + 1 >= 0 && x0 + 1 < n;
+        const bool ya = y0 >= 0 && y0 < n, yb = y0 + 1 >= 0 && y0 + 1 < n;
+        const float* r0 = im + (size_t)y0 * n;
+        double v = 0.0;
+        if (ya) {
+          if (xa) v += (1.0 - wx) * (1.0 - wy) * (double)__ldg(r0 + x0);
+          if (xb) v += wx * (1.0 - wy) * (double)__ldg(r0 + x0 + 1);
+        }
+        if (yb) {
+          if (xa) v += (1.0 - wx) * wy * (double)__ldg(r0 + n + x0);
+          if (xb) v += wx * wy * (double)__ldg(r0 + n + x0 + 1);
+        }
+        acc += v;
+      }
+    }
+  }
+  sino[((size_t)q * n_ang + j) * p.n_t + i] = (float)(acc * h);
+}
+
 __global__ void __launch_bounds__(256) k5_slant(DevPlan p, const float* __restrict__ rows, int n_ang,
                                                 float* __restrict__ img, float scale, Work w) {
   const int m1 = blockIdx.x * 16 + (threadIdx.x & 15);

@@ -271,6 +271,14 @@ class NativePlan:
                              int(n_slices), ctypes.c_float(scale), self._stream(stream))
         _native.check(rc, "tb_ss")
 
+    def forward(self, image: torch.Tensor, sino: torch.Tensor, n_slices: int, step_length: float = 0.5,
+                nearest: bool = False, stream=None) -> None:
+        """Forward projector (tb_forward): images [B][n][n] -> sinograms [B][A][n_t]."""
+        rc = self._lib.tb_forward(self._h, ctypes.c_void_p(image.data_ptr()), ctypes.c_void_p(sino.data_ptr()),
+                                  int(n_slices), ctypes.c_double(step_length), 1 if nearest else 0,
+                                  self._stream(stream))
+        _native.check(rc, "tb_forward")
+
     def polar(self, workspace: torch.Tensor, batch: int, stream=None) -> torch.Tensor:
         """K1 output of the last launch group (first lane) on this workspace:
         [batch][rows][L/2] complex64 (tb_copy_polar)."""

@@ -75,6 +75,30 @@ def _norm_case(name, y, i0, dark_level, rng, plan_kw=None):
     print(f"{name}: counts {counts.shape} -> {out['fbp_bst'].shape}")
 
 
+def _proj_case(name, img, n_t, n_ang, full_turn=False, cfg_kw=None):
+    """forward_project of an image through the reference (projector.py:94-123)."""
+    from tomoblocks import projector as ref_proj
+    from tomoblocks.grids import ImageGrid
+    cfg_kw = cfg_kw or {}
+    img = np.asarray(img, dtype=np.float32)
+    y = ref_proj.forward_project(ImageGrid(img.shape[0], img.astype(np.float64)), DetectorAxis(n_t),
+                                 AngleAxis(n_ang, full_turn=full_turn), ref_proj.RayTraceConfig(**cfg_kw))
+    os.makedirs(os.path.join(HERE, "proj"), exist_ok=True)
+    np.savez_compressed(os.path.join(HERE, "proj", f"{name}.npz"), image=img, sino=y.data,
+                        params=np.array(json.dumps({"n_t": n_t, "n_angles": n_ang, "full_turn": full_turn,
+                                                    "cfg": cfg_kw})))
+    print(f"{name}: image {img.shape} -> sino {y.data.shape}")
+
+
+def _phantom_image(n, rng):
+    """Two ellipses plus noise on the n x n pixel-centre grid (input synthesis)."""
+    x = -1.0 + (np.arange(n) + 0.5) * 2.0 / n
+    u1, u2 = np.meshgrid(x, x)
+    img = 1.0 * (((u1 - 0.1) / 0.6) ** 2 + ((u2 + 0.05) / 0.45) ** 2 <= 1.0)
+    img += 0.5 * (((u1 + 0.3) / 0.2) ** 2 + ((u2 - 0.2) / 0.3) ** 2 <= 1.0)
+    return img + 0.05 * rng.standard_normal((n, n))
+
+
 def main():
     rng0 = np.random.default_rng(0)
     rng1 = np.random.default_rng(1)
@@ -109,6 +133,11 @@ def main():
     _norm_case("norm_shepp128", ellipse_sinogram(SHEPP_LOGAN, 128, 128) * 0.5, 1.0e4, 100.0, rng2)
     _norm_case("norm_ellipse256x192", ellipse_sinogram([(1.0, 0.5, 0.4, 0.1, -0.05, 0.0)], 256, 192),
                4.0e3, 50.0, rng2, {"output_n": 200})
+    # forward projector: bilinear / nearest / full turn / coarse step
+    rng3 = np.random.default_rng(3)
+    _proj_case("fp_bilinear64", _phantom_image(64, rng3), 80, 90)
+    _proj_case("fp_nearest48", _phantom_image(48, rng3), 50, 36, cfg_kw={"interpolation": "nearest"})
+    _proj_case("fp_fullturn40", _phantom_image(40, rng3), 41, 60, full_turn=True, cfg_kw={"step_length": 1.0})
     import scipy
     with open(os.path.join(HERE, "versions.json"), "w") as f:
         json.dump({"numpy": np.__version__, "scipy": scipy.__version__,
