@@ -13,6 +13,8 @@
  *   tb_fbp_ss                         <- fbp(kernel="ss")          fourier_bp.py:525-527
  *   tb_forward                        <- forward_project           projector.py:94-123
  *   tb_normalize                      <- preprocess.normalize      preprocess.py:59-74
+ *   tb_center_estimate / _apply       <- estimate/apply_center     preprocess.py:88-138
+ *   tb_rings                          <- suppress_rings            preprocess.py:141-154
  *   tb_fbp_counts                     <- normalize + fbp stages    pipeline.py:447-459, 486-518
  *
  * Conventions (grids.py): sinograms are angle-major float32 [B][A][n_t]
@@ -132,6 +134,24 @@ int tb_fbp_counts(const tb_plan* plan, const float* counts, const float* flat, c
  * [B][A][n_t] -> line integrals, same shape.  NaN counts stay NaN. */
 int tb_normalize(const tb_plan* plan, const float* counts, const float* flat, const float* dark,
                  double eps, float* out, int n_slices, void* stream);
+
+/* Rotation-centre estimate per slice (preprocess.estimate_center,
+ * preprocess.py:88-118): beta_conf (device, [B][2] double) receives (beta in
+ * detector bins, confidence); status (device, [B] int) 0 ok, 1 constant
+ * sinogram, 2 implausible shift (the reference's CenteringError cases). */
+int tb_center_estimate(const tb_plan* plan, const float* sino, int n_slices, double* beta_conf,
+                       int* status, void* stream);
+
+/* Undo a per-slice detector shift (preprocess.apply_center, :121-138) with
+ * beta = beta_conf[2 q]; in and out [B][A][n_t] (may not alias). */
+int tb_center_apply(const tb_plan* plan, const float* sino, const double* beta_conf, float* out,
+                    int n_slices, void* stream);
+
+/* Ring suppression (preprocess.suppress_rings, :141-154): subtract the
+ * per-detector mean over angles minus its reflect-padded moving average of
+ * odd `window` >= 3.  scratch: device [B][n_t] doubles.  May not alias. */
+int tb_rings(const tb_plan* plan, const float* sino, float* out, int window, double* scratch,
+             int n_slices, void* stream);
 
 /* BST backprojection only (input already ramp-filtered; no 1/(2 pi)). */
 int tb_bst(const tb_plan* plan, const float* sino, float* image, int n_slices,

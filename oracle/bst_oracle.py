@@ -264,6 +264,62 @@ def forward_project(img: np.ndarray, n_t: int, n_angles: int, full_turn: bool = 
     return out
 
 
+def _parabolic_peak(values: np.ndarray, k: int) -> float:
+    """Sub-sample peak through k-1, k, k+1 (preprocess.py:77-85)."""
+    if k <= 0 or k >= len(values) - 1:
+        return float(k)
+    y0, y1, y2 = values[k - 1], values[k], values[k + 1]
+    denom = y0 - 2.0 * y1 + y2
+    if denom == 0.0:
+        return float(k)
+    return k + 0.5 * (y0 - y2) / denom
+
+
+def estimate_center(y: np.ndarray) -> tuple[float, float]:
+    """(beta, confidence) from the mirror consistency of the first and the
+    reversed last projection: full cross-correlation, first argmax,
+    parabolic refinement, beta = lag / 2 (preprocess.py:88-118).  Raises
+    ValueError where the reference raises CenteringError."""
+    v, n_t = y.shape
+    if v < 2:
+        raise ValueError("need at least two projection angles")
+    a = y[0].astype(float)
+    b = y[-1][::-1].astype(float)
+    a = a - a.mean()
+    b = b - b.mean()
+    norm = np.linalg.norm(a) * np.linalg.norm(b)
+    if norm == 0.0:
+        raise ValueError("centering undetermined: constant sinogram")
+    corr = np.correlate(a, b, mode="full")
+    k = int(np.argmax(corr))
+    beta = (_parabolic_peak(corr, k) - (n_t - 1)) / 2.0
+    if abs(beta) > n_t / 2:
+        raise ValueError(f"implausible center shift of {beta:.1f} bins")
+    return beta, float(np.clip(corr[k] / norm, 0.0, 1.0))
+
+
+def apply_center(y: np.ndarray, beta: float) -> np.ndarray:
+    """Undo a detector shift of beta bins by linear interpolation, zero out
+    of range (preprocess.py:121-138)."""
+    n_t = y.shape[1]
+    idx = np.arange(n_t) + beta
+    i0 = np.floor(idx).astype(np.int64)
+    fr = idx - i0
+    ok0 = (i0 >= 0) & (i0 <= n_t - 1)
+    ok1 = (i0 + 1 >= 0) & (i0 + 1 <= n_t - 1)
+    i0c, i1c = np.clip(i0, 0, n_t - 1), np.clip(i0 + 1, 0, n_t - 1)
+    return y[:, i0c] * np.where(ok0, 1.0 - fr, 0.0) + y[:, i1c] * np.where(ok1, fr, 0.0)
+
+
+def suppress_rings(y: np.ndarray, window: int = 9) -> np.ndarray:
+    """Subtract the angle-constant stripe estimate: per-detector mean over
+    angles minus its reflect-padded moving average (preprocess.py:141-154)."""
+    m = y.mean(axis=0)
+    padded = np.pad(m, window // 2, mode="reflect")
+    smooth = np.convolve(padded, np.full(window, 1.0 / window), mode="valid")
+    return y - (m - smooth)[None, :]
+
+
 def normalize(counts: np.ndarray, flat: np.ndarray, dark: np.ndarray, eps: float = 1e-6) -> np.ndarray:
     """Transmission counts to line integrals, -log(max(I - D, eps) / max(I0 - D, eps))
     (preprocess.py:59-74; np.maximum propagates NaN like the reference)."""

@@ -91,6 +91,9 @@ def _bind(lib):
         "tb_fbp_counts": (I, [P, P, P, P, ctypes.c_double, P, I, I, P, S, P]),
         "tb_normalize": (I, [P, P, P, P, ctypes.c_double, P, I, P]),
         "tb_forward": (I, [P, P, P, I, ctypes.c_double, I, P]),
+        "tb_center_estimate": (I, [P, P, I, P, P, P]),
+        "tb_center_apply": (I, [P, P, P, P, I, P]),
+        "tb_rings": (I, [P, P, P, I, P, I, P]),
         "tb_copy_polar": (I, [P, P, I, P, P]),
         "tb_reset_status": (I, [P, P, P]),
         "tb_read_status": (I, [P, P, P]),

@@ -719,6 +719,72 @@ int tb_forward(const tb_plan* p, const float* image, float* sino, int n_slices, 
   return TB_OK;
 }
 
+namespace {
+int check_rows_call(const tb_plan* p, const void* a, const void* b, int n_slices) {
+  if (!p) return fail(TB_ERR_INVALID, "null plan");
+  if (n_slices < 0) return fail(TB_ERR_INVALID, "n_slices must be >= 0");
+  if (n_slices > 0 && (!a || !b)) return fail(TB_ERR_INVALID, "null data pointer");
+  return TB_OK;
+}
+}  // namespace
+
+int tb_center_estimate(const tb_plan* p, const float* sino, int n_slices, double* beta_conf, int* status,
+                       void* stream) {
+  int rc = check_rows_call(p, sino, beta_conf, n_slices);
+  if (rc) return rc;
+  if (n_slices > 0 && !status) return fail(TB_ERR_INVALID, "null status pointer");
+  if (p->rows < 2) return fail(TB_ERR_INVALID, "need at least two projection angles");
+  if (n_slices == 0) return TB_OK;
+  if ((rc = set_device(p))) return rc;
+  const int T = 512;
+  const size_t sm = (size_t)(4 * p->n_t - 1) * sizeof(double) + (size_t)2 * T * sizeof(double) + (size_t)T * sizeof(int);
+  TB_CUDA(cudaFuncSetAttribute(tb::k_center_estimate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  tb::k_center_estimate<<<n_slices, T, sm, static_cast<cudaStream_t>(stream)>>>(
+      sino, p->rows, p->n_t, reinterpret_cast<double2*>(beta_conf), status);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_center_apply(const tb_plan* p, const float* sino, const double* beta_conf, float* out, int n_slices,
+                    void* stream) {
+  int rc = check_rows_call(p, sino, out, n_slices);
+  if (rc) return rc;
+  if (n_slices > 0 && !beta_conf) return fail(TB_ERR_INVALID, "null beta pointer");
+  if (n_slices == 0) return TB_OK;
+  if ((rc = set_device(p))) return rc;
+  for (int s = 0; s < n_slices; s += 65535) {
+    const int B = std::min(65535, n_slices - s);
+    dim3 grid((p->n_t + 255) / 256, p->rows, B);
+    tb::k_center_apply<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        sino + (size_t)s * p->rows * p->n_t, out + (size_t)s * p->rows * p->n_t,
+        reinterpret_cast<const double2*>(beta_conf) + s, p->rows, p->n_t);
+  }
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_rings(const tb_plan* p, const float* sino, float* out, int window, double* scratch, int n_slices,
+             void* stream) {
+  int rc = check_rows_call(p, sino, out, n_slices);
+  if (rc) return rc;
+  if (window < 3 || window % 2 == 0)
+    return fail(TB_ERR_INVALID, "window must be an odd integer >= 3, got " + std::to_string(window));
+  if (n_slices > 0 && !scratch) return fail(TB_ERR_INVALID, "null scratch pointer");
+  if (n_slices == 0) return TB_OK;
+  if ((rc = set_device(p))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int s = 0; s < n_slices; s += 65535) {
+    const int B = std::min(65535, n_slices - s);
+    dim3 grid((p->n_t + 255) / 256, B);
+    const float* in = sino + (size_t)s * p->rows * p->n_t;
+    tb::k_col_mean<<<grid, 256, 0, st>>>(in, scratch, p->rows, p->n_t);
+    tb::k_rings_apply<<<grid, 256, 0, st>>>(in, out + (size_t)s * p->rows * p->n_t, scratch, p->rows, p->n_t,
+                                             window);
+  }
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
 int tb_fbp_ss(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws,
               size_t ws_bytes, void* stream) {
   int rc = check_exec_args(p, sino, image, n_slices, batch, ws, ws_bytes);

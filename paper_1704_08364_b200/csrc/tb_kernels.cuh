@@ -900,6 +900,146 @@ __global__ void __launch_bounds__(256) k_norm_table(const float* __restrict__ fl
   tab[i] = make_float2(d, 1.f / (den != den ? den : fmaxf(den, eps)));
 }
 
+// ---------------------------------------------------------------------------
+// Centering and ring suppression (preprocess.py:77-154), fp64 arithmetic on
+// fp32 rows like the reference's float64 on float32-valued data.
+// ---------------------------------------------------------------------------
+// one CTA per slice: full cross-correlation of row 0 and the reversed last
+// row (means removed), first argmax, parabolic refinement; out[q] = (beta,
+// confidence), st[q] = 0 ok / 1 constant / 2 implausible.  smem: 4 n_t - 1
+// doubles + the reduction scratch.
+__global__ void __launch_bounds__(512) k_center_estimate(const float* __restrict__ sino, int rows, int n_t,
+                                                         double2* __restrict__ out, int* __restrict__ st) {
+  extern __shared__ double cs_mem[];
+  double* a = cs_mem;
+  double* b = a + n_t;
+  double* corr = b + n_t;               // 2 n_t - 1
+  double* red = corr + 2 * n_t - 1;     // [2 blockDim]
+  int* redi = reinterpret_cast<int*>(red + 2 * blockDim.x);
+  const int q = blockIdx.x, t = threadIdx.x, T = blockDim.x;
+  const float* y = sino + (size_t)q * rows * n_t;
+  double sa = 0.0, sb = 0.0;
+  for (int i = t; i < n_t; i += T) {
+    a[i] = (double)y[i];
+    b[i] = (double)y[(size_t)(rows - 1) * n_t + (n_t - 1 - i)];
+    sa += a[i];
+    sb += b[i];
+  }
+  auto block_sum2 = [&](double& x, double& z) {
+    red[t] = x;
+    red[t + T] = z;
+    __syncthreads();
+    for (int s = T / 2; s > 0; s >>= 1) {
+      if (t < s) {
+        red[t] += red[t + s];
+        red[t + T] += red[t + T + s];
+      }
+      __syncthreads();
+    }
+    x = red[0];
+    z = red[T];
+    __syncthreads();
+  };
+  block_sum2(sa, sb);
+  const double ma = sa / n_t, mb = sb / n_t;
+  double na = 0.0, nb = 0.0;
+  for (int i = t; i < n_t; i += T) {
+    a[i] -= ma;
+    b[i] -= mb;
+    na += a[i] * a[i];
+    nb += b[i] * b[i];
+  }
+  block_sum2(na, nb);
+  const double norm = sqrt(na) * sqrt(nb);
+  // corr[k] = sum_n a[n + k - (n_t - 1)] b[n]   (np.correlate "full")
+  double best = -INFINITY;
+  int bk = 0x7fffffff;
+  for (int k = t; k < 2 * n_t - 1; k += T) {
+    const int s = k - (n_t - 1);
+    const int n0 = max(0, -s), n1 = min(n_t, n_t - s);
+    double c = 0.0;
+    for (int n = n0; n < n1; ++n) c = fma(a[n + s], b[n], c);
+    corr[k] = c;
+    if (c > best) { best = c; bk = k; }  // k increases: ties keep the first
+  }
+  red[t] = best;
+  redi[t] = bk;
+  __syncthreads();
+  for (int s = T / 2; s > 0; s >>= 1) {
+    if (t < s) {
+      const double o = red[t + s];
+      const int oi = redi[t + s];
+      if (o > red[t] || (o == red[t] && oi < redi[t])) { red[t] = o; redi[t] = oi; }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    const int k = redi[0];
+    double pk = (double)k;
+    if (k > 0 && k < 2 * n_t - 2) {
+      const double y0 = corr[k - 1], y1 = corr[k], y2 = corr[k + 1];
+      const double den = y0 - 2.0 * y1 + y2;
+      if (den != 0.0) pk = k + 0.5 * (y0 - y2) / den;
+    }
+    const double beta = (pk - (n_t - 1)) / 2.0;
+    const double conf = norm > 0.0 ? fmin(fmax(corr[k] / norm, 0.0), 1.0) : 0.0;
+    out[q] = make_double2(beta, conf);
+    st[q] = norm == 0.0 ? 1 : (fabs(beta) > n_t / 2.0 ? 2 : 0);
+  }
+}
+
+// out = apply_center(in, beta[q].x): linear interpolation at i + beta, zero
+// out of range (preprocess.py:121-138)
+__global__ void __launch_bounds__(256) k_center_apply(const float* __restrict__ in, float* __restrict__ out,
+                                                      const double2* __restrict__ beta, int rows, int n_t) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y, q = blockIdx.z;
+  if (i >= n_t) return;
+  const double idx = (double)i + beta[q].x;
+  const double fl = floor(idx);
+  const long long i0 = (long long)fl;
+  const double fr = idx - fl;
+  const bool ok0 = i0 >= 0 && i0 <= n_t - 1, ok1 = i0 + 1 >= 0 && i0 + 1 <= n_t - 1;
+  const long long i0c = i0 < 0 ? 0 : (i0 > n_t - 1 ? n_t - 1 : i0);
+  const long long i1c = i0 + 1 < 0 ? 0 : (i0 + 1 > n_t - 1 ? n_t - 1 : i0 + 1);
+  const float* r = in + ((size_t)q * rows + j) * n_t;
+  out[((size_t)q * rows + j) * n_t + i] =
+      (float)((double)r[i0c] * (ok0 ? 1.0 - fr : 0.0) + (double)r[i1c] * (ok1 ? fr : 0.0));
+}
+
+// per-detector mean over angles (fp64), mean[q][i]
+__global__ void __launch_bounds__(256) k_col_mean(const float* __restrict__ in, double* __restrict__ mean, int rows,
+                                                  int n_t) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;
+  if (i >= n_t) return;
+  const float* y = in + (size_t)q * rows * n_t + i;
+  double s = 0.0;
+  for (int j = 0; j < rows; ++j) s += (double)y[(size_t)j * n_t];
+  mean[(size_t)q * n_t + i] = s / rows;
+}
+
+// out = in - (mean - movavg_window(reflect-pad(mean)))  (preprocess.py:141-154)
+__global__ void __launch_bounds__(256) k_rings_apply(const float* __restrict__ in, float* __restrict__ out,
+                                                     const double* __restrict__ mean, int rows, int n_t, int window) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;
+  if (i >= n_t) return;
+  const double* m = mean + (size_t)q * n_t;
+  const int h = window / 2;
+  double acc = 0.0;
+  for (int d = -h; d <= h; ++d) {
+    int k = i + d;
+    // np.pad(mode="reflect"): mirror about the edge samples (edge not repeated)
+    while (k < 0 || k > n_t - 1) k = k < 0 ? -k : 2 * (n_t - 1) - k;
+    acc += m[k] * (1.0 / window);
+  }
+  const double stripe = m[i] - acc;
+  const float* y = in + (size_t)q * rows * n_t + i;
+  float* o = out + (size_t)q * rows * n_t + i;
+  for (int j = 0; j < rows; ++j) o[(size_t)j * n_t] = (float)((double)y[(size_t)j * n_t] - stripe);
+}
+
 // standalone normalize over n slices of [rows][n_t] counts
 __global__ void __launch_bounds__(256) k_normalize(const float* __restrict__ counts, const float* __restrict__ flat,
                                                    const float* __restrict__ dark, float eps, float* __restrict__ out,

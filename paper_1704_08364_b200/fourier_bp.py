@@ -279,6 +279,28 @@ class NativePlan:
                                   self._stream(stream))
         _native.check(rc, "tb_forward")
 
+    def center_estimate(self, sino: torch.Tensor, n_slices: int, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+        """(beta_conf [B][2] float64, status [B] int32) device tensors (tb_center_estimate)."""
+        bc = torch.empty((n_slices, 2), dtype=torch.float64, device=f"cuda:{self.device}")
+        st = torch.empty((n_slices,), dtype=torch.int32, device=f"cuda:{self.device}")
+        rc = self._lib.tb_center_estimate(self._h, ctypes.c_void_p(sino.data_ptr()), int(n_slices),
+                                          ctypes.c_void_p(bc.data_ptr()), ctypes.c_void_p(st.data_ptr()),
+                                          self._stream(stream))
+        _native.check(rc, "tb_center_estimate")
+        return bc, st
+
+    def center_apply(self, sino: torch.Tensor, beta_conf: torch.Tensor, out: torch.Tensor, n_slices: int,
+                     stream=None) -> None:
+        rc = self._lib.tb_center_apply(self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(beta_conf.data_ptr()),
+                                       ctypes.c_void_p(out.data_ptr()), int(n_slices), self._stream(stream))
+        _native.check(rc, "tb_center_apply")
+
+    def rings(self, sino: torch.Tensor, out: torch.Tensor, window: int, n_slices: int, stream=None) -> None:
+        scratch = torch.empty((max(n_slices, 1), self.n_t), dtype=torch.float64, device=f"cuda:{self.device}")
+        rc = self._lib.tb_rings(self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                int(window), ctypes.c_void_p(scratch.data_ptr()), int(n_slices), self._stream(stream))
+        _native.check(rc, "tb_rings")
+
     def polar(self, workspace: torch.Tensor, batch: int, stream=None) -> torch.Tensor:
         """K1 output of the last launch group (first lane) on this workspace:
         [batch][rows][L/2] complex64 (tb_copy_polar)."""
@@ -419,7 +441,7 @@ def _frames_on(frames, dev: int, A: int, n_t: int):
 def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan(), kernel: str = "bst",
                full_turn: bool = False, out: torch.Tensor | None = None, batch: int | None = None,
                devices=None, chunk: int | None = None, check: bool = True, frames=None,
-               eps: float = 1e-6) -> torch.Tensor:
+               eps: float = 1e-6, center=None, rings: int | None = None) -> torch.Tensor:
     """Reconstruct a sinogram volume [S][A][n_t] -> image volume [S][n][n].
 
     * CUDA tensor input: computed on that device, asynchronously on the
@@ -439,6 +461,12 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     (preprocess.py:59-74, pipeline.py:447-459), runs fused into the radial
     kernel's load for kernel "bst" (device or host input), or as a separate
     pass before "ss" / "none" (device input).
+
+    ``center`` ("auto": per-slice estimate_center; a float: that beta for
+    every slice) and ``rings`` (odd window) run the reference pipeline's
+    center and rings stages (pipeline.py:461-484) on the device before the
+    reconstruction (device input); an implausible or undetermined centre
+    raises CenteringError like the reference.
     """
     if frames is not None and not eps > 0:
         raise ValueError("eps must be positive")
@@ -459,6 +487,12 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     n = plan.output_n
     if batch is None:
         batch = default_batch(plan)
+    if (center is not None or rings is not None) and not sino.is_cuda:
+        raise ValueError("center / rings stages run on device-resident volumes")
+    if sino.is_cuda and S and (center is not None or rings is not None):
+        from .preprocess import preprocess_volume
+        sino = preprocess_volume(sino, plan, full_turn, frames=frames, eps=eps, center=center, rings=rings)
+        frames = None  # normalised by the preprocessing pass
     if sino.is_cuda:
         dev = sino.device.index
         nat = native_plan(plan, fplan, full_turn, dev)
