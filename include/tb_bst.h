@@ -16,6 +16,7 @@
  *   tb_center_estimate / _apply       <- estimate/apply_center     preprocess.py:88-138
  *   tb_rings                          <- suppress_rings            preprocess.py:141-154
  *   tb_fbp_counts                     <- normalize + fbp stages    pipeline.py:447-459, 486-518
+ *   tb_fbp_frames                     <- read (layout 0) + fbp     volio.py:159-180, pipeline.py:486-518
  *
  * Conventions (grids.py): sinograms are angle-major float32 [B][A][n_t]
  * (A = n_theta, or 2*n_theta for full-turn input); images are float32
@@ -129,6 +130,12 @@ int tb_fbp_profiled(const tb_plan* plan, const float* sino, float* image, int n_
 int tb_fbp_counts(const tb_plan* plan, const float* counts, const float* flat, const float* dark,
                   double eps, float* image, int n_slices, int batch, void* workspace,
                   size_t workspace_bytes, void* stream);
+
+/* fbp of a frame-major slab [A][n_slices][n_t] (a TOMOVOL1 layout-0 block as
+ * read from disk, volio.py:159-180): the radial kernel reads rows at the
+ * frame stride, so no transpose pass; output [n_slices][n][n]. */
+int tb_fbp_frames(const tb_plan* plan, const float* frames, float* image, int n_slices, int batch,
+                  void* workspace, size_t workspace_bytes, void* stream);
 
 /* normalize alone (preprocess.normalize, preprocess.py:59-74): counts
  * [B][A][n_t] -> line integrals, same shape.  NaN counts stay NaN. */

@@ -16,7 +16,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # lazy: importing torch-backed modules only when the API is used
-    if name in ("fourier_bp", "projector", "pipeline", "phantom", "preprocess", "slabs"):
+    if name in ("fourier_bp", "projector", "pipeline", "phantom", "preprocess", "slabs", "volio"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

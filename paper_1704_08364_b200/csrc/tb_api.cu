@@ -108,6 +108,8 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   w.status = reinterpret_cast<int*>(static_cast<char*>(ws) + l.status);
   w.normtab = nullptr;
   w.norm_eps = 0.f;
+  w.in_slice = (long long)p->rows * p->n_t;  // slice-major input by default
+  w.in_row = p->n_t;
   w.groups = p->groups;
   w.pairs_per_cta = p->pairs_per_cta;
   w.polar_tex = polar_texture(p, w.polar, B * p->dp.prow);
@@ -209,7 +211,7 @@ struct NormFrames {
 
 int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, int batch, void* ws,
                  size_t ws_bytes, void* stream, bool ramp, float scale, double* stage_ms = nullptr,
-                 const NormFrames* norm = nullptr) {
+                 const NormFrames* norm = nullptr, bool frame_major = false) {
   int rc = check_exec_args(p, sino, img, n_slices, batch, ws, ws_bytes);
   if (rc) return rc;
   if ((rc = set_device(p))) return rc;
@@ -221,7 +223,10 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
     tb::k_norm_table<<<(cnt + 255) / 256, 256, 0, st>>>(norm->flat, norm->dark, (float)norm->eps, normtab, cnt);
     TB_CUDA(cudaGetLastError());
   }
-  const size_t in_stride = (size_t)p->rows * p->n_t;
+  // frame-major input [A][n_slices][n_t] (a TOMOVOL1 layout-0 slab): slice
+  // q, row j at q n_t + j n_slices n_t -- read in place, no transpose
+  const size_t in_stride = frame_major ? (size_t)p->n_t : (size_t)p->rows * p->n_t;
+  const long long in_row = frame_major ? (long long)n_slices * p->n_t : (long long)p->n_t;
   const size_t out_stride = (size_t)p->n * p->n;
   const int ngroups = (n_slices + batch - 1) / batch;
   std::vector<cudaEvent_t> evs;
@@ -252,6 +257,8 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
     const int B = std::min(batch, n_slices - s0);
     const int lane = g % lanes;
     Work w = work_for(p, batch, ws, lane);
+    w.in_slice = (long long)in_stride;
+    w.in_row = in_row;
     if (norm) {
       w.normtab = normtab;
       w.norm_eps = (float)norm->eps;
@@ -637,6 +644,12 @@ int tb_fbp_counts(const tb_plan* p, const float* counts, const float* flat, cons
                       nullptr, &nf);
 }
 
+int tb_fbp_frames(const tb_plan* p, const float* frames, float* image, int n_slices, int batch, void* ws,
+                  size_t ws_bytes, void* stream) {
+  return run_bst_like(p, frames, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)),
+                      nullptr, nullptr, true);
+}
+
 int tb_normalize(const tb_plan* p, const float* counts, const float* flat, const float* dark, double eps, float* out,
                  int n_slices, void* stream) {
   if (!p) return fail(TB_ERR_INVALID, "null plan");
@@ -669,6 +682,8 @@ int tb_ramp(const tb_plan* p, const float* sino, float* out, int n_slices, void*
   if (rc) return rc;
   Work w{};
   w.status = nullptr;
+  w.in_slice = (long long)p->rows * p->n_t;
+  w.in_row = p->n_t;
   return ramp_dispatch(p, sino, out, n_slices * p->rows, w, static_cast<cudaStream_t>(stream));
 }
 

@@ -64,6 +64,9 @@ struct Work {
   // (dark D, 1 / max(I0 - D, eps)) and eps
   const float2* normtab;
   float norm_eps;
+  // input addressing (elements): row j of slice q at q * in_slice + j * in_row
+  // (slice-major [B][A][n_t]: A n_t, n_t; a frame-major slab [A][B][n_t]: n_t, B n_t)
+  long long in_slice, in_row;
   int groups;   // K1 CTAs per slice (partial-sum groups)
   int pairs_per_cta;
   // texture view of this lane's polar region (pitch 2D, float2 texels,
@@ -119,15 +122,22 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
   const int pr_begin = g * w.pairs_per_cta;
   const int pr_end = min(npairs, pr_begin + w.pairs_per_cta);
   const int H = L / 2;
-  const float* slice = sino + (size_t)q * p.rows * p.n_t;
+  const float* slice = sino + (size_t)q * w.in_slice;
   // bulk copies need 16-byte aligned rows; otherwise read rows directly
-  const bool bulk = (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0);
+  const bool bulk = (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0) && (w.in_row & 3) == 0 &&
+                    (w.in_slice & 3) == 0;
   auto issue = [&](int pr, int slot) {
     const int j0 = 2 * pr;
     const int nrow = (2 * pr + 1 < p.rows) ? 2 : 1;
     const uint32_t bytes = (uint32_t)(nrow * p.n_t * 4);
     mbar_expect_tx(&bars[slot], bytes);
-    bulk_g2s(stage + slot * 2 * p.n_t, slice + (size_t)j0 * p.n_t, bytes, &bars[slot]);
+    if (w.in_row == p.n_t) {  // the pair is one contiguous run
+      bulk_g2s(stage + slot * 2 * p.n_t, slice + (size_t)j0 * p.n_t, bytes, &bars[slot]);
+    } else {
+      const uint32_t rb = (uint32_t)(p.n_t * 4);
+      bulk_g2s(stage + slot * 2 * p.n_t, slice + (size_t)j0 * w.in_row, rb, &bars[slot]);
+      if (nrow == 2) bulk_g2s(stage + slot * 2 * p.n_t + p.n_t, slice + (size_t)(j0 + 1) * w.in_row, rb, &bars[slot]);
+    }
   };
 
   for (int i = t; i < p.S; i += blockDim.x) sacc[i] = 0.f;
@@ -171,8 +181,8 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
         v[i] = make_float2(a, b);
       }
     } else {
-      const float* y0 = slice + (size_t)j0 * p.n_t;
-      const float* y1 = y0 + p.n_t;
+      const float* y0 = slice + (size_t)j0 * w.in_row;
+      const float* y1 = y0 + w.in_row;
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const int idx = t + i * TPF;
@@ -279,8 +289,9 @@ __global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const 
   const bool active = t < TPF;
   const int j0 = 2 * blockIdx.x, j1 = j0 + 1;
   const bool has1 = j1 < total_rows;
-  const float* y0 = sino + (size_t)j0 * p.n_t;
-  const float* y1 = y0 + p.n_t;
+  // global row index j over B slices -> (slice j / rows, row j % rows)
+  const float* y0 = sino + (size_t)(j0 / p.rows) * w.in_slice + (size_t)(j0 % p.rows) * w.in_row;
+  const float* y1 = sino + (size_t)(j1 / p.rows) * w.in_slice + (size_t)(j1 % p.rows) * w.in_row;
   float2 v[RPT];
   bool bad = false;
 #pragma unroll

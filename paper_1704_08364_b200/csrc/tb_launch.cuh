@@ -101,6 +101,7 @@ struct Launch {
                        float out_scale, cudaStream_t st, cudaEvent_t* ev) {
     const DevPlan& dp = p->dp;
     const float* k1_in = sino;
+    Work wk = w;  // K1's view of its input (the filtered rows are slice-major)
     bool fused = false;
     auto mark = [&](int stage, int which) {
       if (ev) cudaEventRecord(ev[2 * stage + which], st);
@@ -114,16 +115,19 @@ struct Launch {
         mark(0, 1);
         if (rc) return rc;
         k1_in = w.filtered;
+        wk.in_slice = (long long)p->rows * p->n_t;
+        wk.in_row = p->n_t;
+        wk.normtab = nullptr;  // normalised by the ramp pass
       }
     }
     dim3 g1(p->groups, B);
     mark(1, 0);
-    if (fused && w.normtab)  // transmission counts: normalisation fused into the load
-      tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+    if (fused && wk.normtab)  // transmission counts: normalisation fused into the load
+      tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else if (fused)
-      tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+      tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else
-      tb::k1_radial<L, false, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, w);
+      tb::k1_radial<L, false, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     mark(1, 1);
     mark(2, 0);
     tb::k1b_common<L><<<B, K::K1B_THREADS, smem_k1b(p), st>>>(dp, w);

@@ -226,7 +226,8 @@ class NativePlan:
 
     def run(self, op: str, sino: torch.Tensor, image: torch.Tensor, n_slices: int, batch: int,
             workspace: torch.Tensor, stream=None) -> None:
-        fn = {"fbp": self._lib.tb_fbp, "bst": self._lib.tb_bst, "fbp_ss": self._lib.tb_fbp_ss}[op]
+        fn = {"fbp": self._lib.tb_fbp, "bst": self._lib.tb_bst, "fbp_ss": self._lib.tb_fbp_ss,
+              "fbp_frames": self._lib.tb_fbp_frames}[op]
         rc = fn(self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(image.data_ptr()), int(n_slices),
                 int(batch), ctypes.c_void_p(workspace.data_ptr()), ctypes.c_size_t(workspace.numel()),
                 self._stream(stream))

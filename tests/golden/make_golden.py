@@ -121,6 +121,30 @@ def _pre_case(name, y, beta_true, window=9):
     print(f"{name}: beta {cr.beta:.4f} (true {beta_true}) conf {cr.confidence:.3f}")
 
 
+def _vol_cases():
+    """TOMOVOL1 bytes from the reference writer and blocks from its reader
+    (volio.py:96-222) for the container round-trip tests."""
+    from tomoblocks import volio as ref_vol
+    from tomoblocks.grids import ImageGrid
+    d = os.path.join(HERE, "vol")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(5)
+    frames = rng.standard_normal((6, 5, 8)).astype(np.float32)  # [angle][slice][det]
+    ref_vol.write_volume(os.path.join(d, "frames.tomovol"), ref_vol.VolumeHeader(0, frames.shape), frames)
+    slices = np.ascontiguousarray(frames.transpose(1, 0, 2))
+    ref_vol.write_volume(os.path.join(d, "slices.tomovol"), ref_vol.VolumeHeader(1, slices.shape), slices)
+    with ref_vol.BlockReader(os.path.join(d, "frames.tomovol"), 2) as rd:
+        blocks = [np.stack([s.data for s in b.slices]) for b in rd]
+    imgs = rng.standard_normal((3, 4, 4))
+    with ref_vol.VolumeWriter(os.path.join(d, "written.tomovol"), 3, 4) as wr:
+        for k in (2, 0, 1):
+            wr.write_slice(k, ImageGrid(4, imgs[k]))
+    ref_vol.export_image(ImageGrid(4, imgs[0]), os.path.join(d, "img0.pgm"))
+    np.savez_compressed(os.path.join(d, "expect.npz"), frames=frames, imgs=imgs,
+                        block0=blocks[0], block1=blocks[1], block2=blocks[2])
+    print("vol: frames/slices/written containers")
+
+
 def main():
     rng0 = np.random.default_rng(0)
     rng1 = np.random.default_rng(1)
@@ -163,6 +187,7 @@ def main():
     # centering + ring suppression
     _pre_case("pre_shepp128", ellipse_sinogram(SHEPP_LOGAN, 128, 128), 3.3)
     _pre_case("pre_ellipse200x90", ellipse_sinogram([(1.0, 0.5, 0.4, 0.1, -0.05, 0.0)], 200, 90), -5.75, 7)
+    _vol_cases()
     import scipy
     with open(os.path.join(HERE, "versions.json"), "w") as f:
         json.dump({"numpy": np.__version__, "scipy": scipy.__version__,
