@@ -311,7 +311,8 @@ def run_ours(args):
     if not args.no_counts and S > 0:
         from paper_1704_08364_b200.preprocess import preprocess_volume
         k = min(S, 64)
-        samp = sino[:k]
+        m0 = max(0, S // 2 - k // 2)  # central slices: the phantom's end slices are empty (undetermined centre)
+        samp = sino[m0:m0 + k]
         preprocess_volume(samp, plan, center="auto", rings=9)  # warm-up
         torch.cuda.synchronize()
         p0, p1, p2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))

@@ -409,16 +409,17 @@ def fbp(y: Sinogram, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
 
 
 def default_batch(plan: BstPlan) -> int:
-    """Slices per launch group (two groups in flight on two streams): enough
-    CTAs to fill 148 SMs for small slices; 4 slices at L = 4096 (measured
-    best of 1/2/4/8 x lanes 1-4, profiles/README.md) keeps the K1 -> K2 -> K3
-    intermediates of the groups in flight near L2 size."""
+    """Slices per launch group (two groups in flight on two streams).  Larger
+    groups fill the 148 SMs with fewer wave tails: at L = 4096 the measured
+    step falls from 218 ms (4 slices) to 204 ms (24-31 slices,
+    profiles/README.md).  Bounded by the polar texture's height,
+    batch * (n_theta + 1) <= 65000 rows (31 slices at 2048 angles), and at
+    64 slices."""
     L = plan.radial_samples
-    if L >= 4096:
-        return 4
-    if L >= 2048:
-        return 8
-    return max(1, min(64, (4096 // L) ** 2))
+    rows = plan.n_theta + 1
+    if L >= 1024:
+        return max(1, min(64, 65000 // rows))
+    return max(1, min(64, (4096 // L) ** 2, 65000 // rows))
 
 
 def _split(n: int, parts: int) -> list[tuple[int, int]]:
