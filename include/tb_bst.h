@@ -131,6 +131,12 @@ int tb_fbp_counts(const tb_plan* plan, const float* counts, const float* flat, c
                   double eps, float* image, int n_slices, int batch, void* workspace,
                   size_t workspace_bytes, void* stream);
 
+/* tb_fbp_counts for constant frames (the reference pipeline's i0 / dark
+ * scalars, pipeline.py:447-451): no per-sample frame loads. */
+int tb_fbp_counts_const(const tb_plan* plan, const float* counts, double i0, double dark,
+                        double eps, float* image, int n_slices, int batch, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
 /* fbp of a frame-major slab [A][n_slices][n_t] (a TOMOVOL1 layout-0 block as
  * read from disk, volio.py:159-180): the radial kernel reads rows at the
  * frame stride, so no transpose pass; output [n_slices][n][n]. */

@@ -90,6 +90,7 @@ def _bind(lib):
         "tb_fbp_ss": (I, [P, P, P, I, I, P, S, P]),
         "tb_fbp_counts": (I, [P, P, P, P, ctypes.c_double, P, I, I, P, S, P]),
         "tb_fbp_frames": (I, [P, P, P, I, I, P, S, P]),
+        "tb_fbp_counts_const": (I, [P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, P, I, I, P, S, P]),
         "tb_normalize": (I, [P, P, P, P, ctypes.c_double, P, I, P]),
         "tb_forward": (I, [P, P, P, I, ctypes.c_double, I, P]),
         "tb_center_estimate": (I, [P, P, I, P, P, P]),

@@ -108,6 +108,7 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   w.status = reinterpret_cast<int*>(static_cast<char*>(ws) + l.status);
   w.normtab = nullptr;
   w.norm_eps = 0.f;
+  w.norm_c = make_float2(0.f, 0.f);
   w.in_slice = (long long)p->rows * p->n_t;  // slice-major input by default
   w.in_row = p->n_t;
   w.groups = p->groups;
@@ -204,9 +205,10 @@ int set_device(const tb_plan* p) {
 
 // transmission-count input (tb_fbp_counts): flat / dark frames [rows][n_t]
 struct NormFrames {
-  const float* flat;
+  const float* flat;  // null: constant frames i0 / d below
   const float* dark;
   double eps;
+  double i0, d;
 };
 
 int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, int batch, void* ws,
@@ -217,11 +219,15 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
   if ((rc = set_device(p))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* normtab = nullptr;
-  if (norm) {  // (D, 1 / max(I0 - D, eps)) once per call, read by every slice's K1
+  float2 norm_c = make_float2(0.f, 0.f);
+  if (norm && norm->flat) {  // (D, 1 / max(I0 - D, eps)) once per call, read by every slice's K1
     normtab = reinterpret_cast<float2*>(static_cast<char*>(ws) + layout_for(p, batch).normtab);
     const int cnt = p->rows * p->n_t;
     tb::k_norm_table<<<(cnt + 255) / 256, 256, 0, st>>>(norm->flat, norm->dark, (float)norm->eps, normtab, cnt);
     TB_CUDA(cudaGetLastError());
+  } else if (norm) {  // constant frames: the same pair for every sample, no table loads
+    const double den = norm->i0 - norm->d;
+    norm_c = make_float2((float)norm->d, (float)(1.0 / (den != den ? den : std::max(den, norm->eps))));
   }
   // frame-major input [A][n_slices][n_t] (a TOMOVOL1 layout-0 slab): slice
   // q, row j at q n_t + j n_slices n_t -- read in place, no transpose
@@ -262,6 +268,7 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
     if (norm) {
       w.normtab = normtab;
       w.norm_eps = (float)norm->eps;
+      w.norm_c = norm_c;
     }
     cudaStream_t ls = lane ? aux[lane] : st;
     rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, ls,
@@ -639,7 +646,15 @@ int tb_fbp_counts(const tb_plan* p, const float* counts, const float* flat, cons
                   float* image, int n_slices, int batch, void* ws, size_t ws_bytes, void* stream) {
   if (!(eps > 0.0)) return fail(TB_ERR_INVALID, "eps must be positive");
   if (n_slices > 0 && (!flat || !dark)) return fail(TB_ERR_INVALID, "null flat/dark frame");
-  const NormFrames nf{flat, dark, eps};
+  const NormFrames nf{flat, dark, eps, 0.0, 0.0};
+  return run_bst_like(p, counts, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)),
+                      nullptr, &nf);
+}
+
+int tb_fbp_counts_const(const tb_plan* p, const float* counts, double i0, double dark, double eps, float* image,
+                        int n_slices, int batch, void* ws, size_t ws_bytes, void* stream) {
+  if (!(eps > 0.0)) return fail(TB_ERR_INVALID, "eps must be positive");
+  const NormFrames nf{nullptr, nullptr, eps, i0, dark};
   return run_bst_like(p, counts, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)),
                       nullptr, &nf);
 }

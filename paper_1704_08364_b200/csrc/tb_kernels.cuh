@@ -62,8 +62,9 @@ struct Work {
   int* status;  // [0] non-finite input, [1] non-finite output
   // transmission-count input (NORM kernels): per input row and detector
   // (dark D, 1 / max(I0 - D, eps)) and eps
-  const float2* normtab;
+  const float2* normtab;  // null with NORM: constant frames, norm_c = (D, 1 / max(I0 - D, eps))
   float norm_eps;
+  float2 norm_c;
   // input addressing (elements): row j of slice q at q * in_slice + j * in_row
   // (slice-major [B][A][n_t]: A n_t, n_t; a frame-major slab [A][B][n_t]: n_t, B n_t)
   long long in_slice, in_row;
@@ -173,9 +174,14 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
           if (has1) b = r1[idx];
           bad |= !isfinite(a) || !isfinite(b);
           if constexpr (NORM) {
-            const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
-            a = norm_line(a, __ldg(nt), w.norm_eps);
-            if (has1) b = norm_line(b, __ldg(nt + p.n_t), w.norm_eps);
+            if (w.normtab) {
+              const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
+              a = norm_line(a, __ldg(nt), w.norm_eps);
+              if (has1) b = norm_line(b, __ldg(nt + p.n_t), w.norm_eps);
+            } else {
+              a = norm_line(a, w.norm_c, w.norm_eps);
+              if (has1) b = norm_line(b, w.norm_c, w.norm_eps);
+            }
           }
         }
         v[i] = make_float2(a, b);
@@ -194,9 +200,14 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
           if (has1) b = __ldg(y1 + idx);
           bad |= !isfinite(a) || !isfinite(b);
           if constexpr (NORM) {
-            const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
-            a = norm_line(a, __ldg(nt), w.norm_eps);
-            if (has1) b = norm_line(b, __ldg(nt + p.n_t), w.norm_eps);
+            if (w.normtab) {
+              const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
+              a = norm_line(a, __ldg(nt), w.norm_eps);
+              if (has1) b = norm_line(b, __ldg(nt + p.n_t), w.norm_eps);
+            } else {
+              a = norm_line(a, w.norm_c, w.norm_eps);
+              if (has1) b = norm_line(b, w.norm_c, w.norm_eps);
+            }
           }
         }
         v[i] = make_float2(a, b);
@@ -304,9 +315,12 @@ __global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const 
       bad |= !isfinite(a) || !isfinite(b);
       if constexpr (NORM) {
         // input row j0 of slice (j0 / rows) -> frame row j0 % rows
-        const float2* nt = w.normtab + (size_t)(j0 % p.rows) * p.n_t + idx;
-        a = norm_line(a, __ldg(nt), w.norm_eps);
-        if (has1) b = norm_line(b, __ldg(w.normtab + (size_t)(j1 % p.rows) * p.n_t + idx), w.norm_eps);
+        const float2 c0 = w.normtab ? __ldg(w.normtab + (size_t)(j0 % p.rows) * p.n_t + idx) : w.norm_c;
+        a = norm_line(a, c0, w.norm_eps);
+        if (has1) {
+          const float2 c1 = w.normtab ? __ldg(w.normtab + (size_t)(j1 % p.rows) * p.n_t + idx) : w.norm_c;
+          b = norm_line(b, c1, w.norm_eps);
+        }
       }
     }
     v[i] = make_float2(a, b);

@@ -118,11 +118,12 @@ struct Launch {
         wk.in_slice = (long long)p->rows * p->n_t;
         wk.in_row = p->n_t;
         wk.normtab = nullptr;  // normalised by the ramp pass
+        wk.norm_eps = 0.f;
       }
     }
     dim3 g1(p->groups, B);
     mark(1, 0);
-    if (fused && wk.normtab)  // transmission counts: normalisation fused into the load
+    if (fused && wk.norm_eps > 0.f)  // transmission counts: normalisation fused into the load
       tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else if (fused)
       tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
@@ -158,7 +159,7 @@ struct Launch {
 template <int NP>
 int launch_ramp(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
   using K = tb::KShape<NP>;
-  if (w.normtab)  // unfused ramp on transmission counts: normalisation in its load
+  if (w.norm_eps > 0.f)  // unfused ramp on transmission counts: normalisation in its load
     tb::kr_ramp<NP, true><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);
   else
     tb::kr_ramp<NP, false><<<(total_rows + 1) / 2, K::THREADS, K::BUF * sizeof(float2), st>>>(p->dp, in, out, total_rows, w);

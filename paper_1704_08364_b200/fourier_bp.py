@@ -244,6 +244,24 @@ class NativePlan:
                                      self._stream(stream))
         _native.check(rc, "tb_fbp_counts")
 
+    def run_counts_const(self, counts: torch.Tensor, i0: float, dark: float, eps: float, image: torch.Tensor,
+                         n_slices: int, batch: int, workspace: torch.Tensor, stream=None) -> None:
+        """run_counts for constant frames (tb_fbp_counts_const: no frame loads)."""
+        rc = self._lib.tb_fbp_counts_const(self._h, ctypes.c_void_p(counts.data_ptr()), ctypes.c_double(i0),
+                                           ctypes.c_double(dark), ctypes.c_double(eps),
+                                           ctypes.c_void_p(image.data_ptr()), int(n_slices), int(batch),
+                                           ctypes.c_void_p(workspace.data_ptr()), ctypes.c_size_t(workspace.numel()),
+                                           self._stream(stream))
+        _native.check(rc, "tb_fbp_counts_const")
+
+    def counts(self, counts: torch.Tensor, frames, eps: float, image: torch.Tensor, n_slices: int, batch: int,
+               workspace: torch.Tensor, stream=None) -> None:
+        """fbp of counts with `frames` = (flat, dark) device tensors or ("const", i0, dark)."""
+        if frames[0] == "const":
+            self.run_counts_const(counts, frames[1], frames[2], eps, image, n_slices, batch, workspace, stream)
+        else:
+            self.run_counts(counts, frames[0], frames[1], eps, image, n_slices, batch, workspace, stream)
+
     def normalize(self, counts: torch.Tensor, flat: torch.Tensor, dark: torch.Tensor, eps: float,
                   out: torch.Tensor, n_slices: int, stream=None) -> None:
         rc = self._lib.tb_normalize(self._h, ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(flat.data_ptr()),
@@ -428,6 +446,17 @@ def _split(n: int, parts: int) -> list[tuple[int, int]]:
     return split(n, parts)
 
 
+def _counts_frames(frames, dev: int, A: int, n_t: int):
+    """Frames for NativePlan.counts: ("const", i0, dark) when both frames are
+    constant (the reference pipeline's scalar i0 / dark, pipeline.py:447-451),
+    else (flat, dark) device tensors."""
+    f, d = frames.flat, frames.dark
+    if (isinstance(f, np.ndarray) and isinstance(d, np.ndarray) and f.size and f.shape == (A, n_t)
+            and d.shape == (A, n_t) and f.min() == f.max() and d.min() == d.max()):
+        return ("const", float(f.flat[0]), float(d.flat[0]))
+    return tuple(_frames_on(frames, dev, A, n_t))
+
+
 def _frames_on(frames, dev: int, A: int, n_t: int):
     """(flat, dark) of a FlatDarkFrames as float32 [A][n_t] tensors on cuda:dev."""
     out = []
@@ -504,10 +533,10 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
         with torch.cuda.device(dev):
             nat.reset_status(ws)
             if S and frames is not None:
-                flat, dark = _frames_on(frames, dev, A, n_t)
                 if op == "fbp":
-                    nat.run_counts(sino, flat, dark, eps, out, S, min(batch, S), ws)
+                    nat.counts(sino, _counts_frames(frames, dev, A, n_t), eps, out, S, min(batch, S), ws)
                 else:
+                    flat, dark = _frames_on(frames, dev, A, n_t)
                     line = torch.empty_like(sino)
                     nat.normalize(sino, flat, dark, eps, line, S)
                     nat.run(op, line, out, S, min(batch, S), ws)
@@ -553,7 +582,7 @@ def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, c
                 "cmp": [torch.cuda.Event() for _ in range(2)],
                 "d2h": [torch.cuda.Event() for _ in range(2)],
                 "k": 0, "chunk": m,
-                "frames": _frames_on(frames, dev, A, n_t) if frames is not None else None,
+                "frames": _counts_frames(frames, dev, A, n_t) if frames is not None else None,
             }
             nat.reset_status(st["ws"], st["s_cmp"])
         states.append(st)
@@ -576,8 +605,8 @@ def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, c
                 st["s_cmp"].wait_event(st["h2d"][k])
                 st["s_cmp"].wait_event(st["d2h"][k])  # output buffer k free
                 if st["frames"] is not None:
-                    st["nat"].run_counts(st["inb"][k], *st["frames"], eps, st["outb"][k], m, min(batch, st["chunk"]),
-                                         st["ws"], st["s_cmp"])
+                    st["nat"].counts(st["inb"][k], st["frames"], eps, st["outb"][k], m, min(batch, st["chunk"]),
+                                     st["ws"], st["s_cmp"])
                 else:
                     st["nat"].run(op, st["inb"][k], st["outb"][k], m, min(batch, st["chunk"]), st["ws"], st["s_cmp"])
                 st["cmp"][k].record(st["s_cmp"])

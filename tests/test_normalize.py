@@ -98,3 +98,25 @@ def test_gpu_counts_nonfinite_raises():
     counts[0, 7, 9] = float("nan")
     with pytest.raises(ValueError):
         F.fbp_volume(counts, F.BstPlan(n_t, v), frames=FlatDarkFrames(c["flat"], c["dark"]))
+
+
+@pytest.mark.gpu
+def test_gpu_constant_frames_scalar_path_matches_table_path():
+    """Constant frames (the reference pipeline's i0 / dark scalars) take the
+    table-free kernel path; it equals the per-sample table path."""
+    torch = _cuda()
+    from paper_1704_08364_b200 import fourier_bp as F
+    from paper_1704_08364_b200.preprocess import FlatDarkFrames
+    rng = np.random.default_rng(9)
+    v, n_t = 96, 128
+    counts = torch.from_numpy((1e4 * np.exp(-rng.random((2, v, n_t))) + 100.0).astype(np.float32)).cuda()
+    plan = F.BstPlan(n_t, v)
+    const = FlatDarkFrames(np.full((v, n_t), 1e4 + 100.0), np.full((v, n_t), 100.0))
+    a = F.fbp_volume(counts, plan, frames=const)
+    nat = F.native_plan(plan, F.FilterPlan(), False, 0)
+    fl, dk = F._frames_on(const, 0, v, n_t)
+    b = torch.empty_like(a)
+    ws = nat.new_workspace(2)
+    nat.run_counts(counts, fl, dk, 1e-6, b, 2, 2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
