@@ -73,6 +73,8 @@ struct Launch {
   static size_t smem_k2() { return (size_t)K2::G * K2::SMEM_PER_GROUP * sizeof(float2); }
   // columns per K2 CTA: one resident CTA per SM sweeping G columns at a time
   static int k2_cols(const tb_plan* p) {
+    if (const char* e = std::getenv("TB_K2_COLS"))  // tuning: columns swept per CTA
+      if (std::atoi(e) > 0) return K2::G * std::atoi(e);
     const int resident = K2::MINB;  // CTAs per SM
     const int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
     return K2::G * std::max(1, steps);
