@@ -143,6 +143,13 @@ struct Dft {
 };
 
 __device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
+// spad(i + c) for a compile-time c that is a multiple of 16: spad(i) + 17 c / 16
+// (lets every buffer access share one per-thread base + an immediate offset)
+template <int C>
+__device__ __forceinline__ int spad_add(int sp_i) {
+  static_assert(C % 16 == 0, "offset must be a multiple of 16");
+  return sp_i + C + C / 16;
+}
 
 // --- bulk async copy (TMA 1D: cp.async.bulk) with mbarrier completion -------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -203,12 +210,21 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
   constexpr bool FIRST = PASS == 0;
   constexpr bool LAST = PASS == S::NPASS - 1;
   float2 x[PER][R];
+  // loads t + b TPF + m NB: one padded base per thread when TPF and NB are
+  // multiples of 16 (N >= 256), else the padding per element
+  constexpr bool ALIGNED = (S::TPF % 16 == 0) && (NB % 16 == 0);
+  const int sp_t = spad(t);
 #pragma unroll
   for (int b = 0; b < PER; ++b)
 #pragma unroll
     for (int m = 0; m < R; ++m) {
-      if constexpr (FIRST) x[b][m] = v[b + m * PER];
-      else x[b][m] = active ? buf[spad(t + b * S::TPF + m * NB)] : make_float2(0.f, 0.f);
+      if constexpr (FIRST) {
+        x[b][m] = v[b + m * PER];
+      } else if constexpr (ALIGNED) {
+        x[b][m] = active ? buf[sp_t + (b * S::TPF + m * NB) + (b * S::TPF + m * NB) / 16] : make_float2(0.f, 0.f);
+      } else {
+        x[b][m] = active ? buf[spad(t + b * S::TPF + m * NB)] : make_float2(0.f, 0.f);
+      }
     }
   if constexpr (!FIRST) __syncthreads();
 #pragma unroll
@@ -244,8 +260,16 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
       for (int m = 0; m < R; ++m) v[b + m * PER] = x[b][m];
     } else if (active) {
       const int base = (j / NS) * NS * R + k;
+      if constexpr (NS % 16 == 0 || (NS == 1 && R == 16)) {
+        // base + m NS never carries into the padding index beyond m NS / 16
+        // (NS % 16 == 0), or base is a multiple of 16 and m < 16 (NS == 1)
+        const int sp_b = spad(base);
 #pragma unroll
-      for (int m = 0; m < R; ++m) buf[spad(base + m * NS)] = x[b][m];
+        for (int m = 0; m < R; ++m) buf[sp_b + m * NS + (m * NS) / 16] = x[b][m];
+      } else {
+#pragma unroll
+        for (int m = 0; m < R; ++m) buf[spad(base + m * NS)] = x[b][m];
+      }
     }
   }
   if constexpr (!LAST) __syncthreads();

@@ -237,7 +237,14 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
     }
     fft<L, false>(v, buf, t, active, p.tw_L);
     // exchange Z_k / Z_{L-k} through smem to separate the two real rows
-    if constexpr (FftShape<L>::SMEM > 0) {
+    constexpr bool XALIGN = FftShape<L>::SMEM > 0 && (TPF % 16 == 0);
+    if constexpr (XALIGN) {
+      const int sp_t = spad(t);
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) buf[sp_t + i * TPF + (i * TPF) / 16] = v[i];
+      }
+    } else if constexpr (FftShape<L>::SMEM > 0) {
       if (active) {
 #pragma unroll
         for (int i = 0; i < RPT; ++i) buf[spad(t + i * TPF)] = v[i];
@@ -262,7 +269,14 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
         if (k < H) {
           const int km = (L - k) & (L - 1);
           const float2 zk = v[i];
-          const float2 zm = buf[FftShape<L>::SMEM > 0 ? spad(km) : km];
+          float2 zm;
+          if constexpr (XALIGN) {
+            // spad(L - t - i TPF) = spad(-t) + (L - i TPF) 17 / 16 for k > 0
+            const int c = L - i * TPF;
+            zm = k == 0 ? buf[0] : buf[(-t) + ((-t) >> 4) + c + c / 16];
+          } else {
+            zm = buf[FftShape<L>::SMEM > 0 ? spad(km) : km];
+          }
           const float2 X = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
           const float2 Y = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
           const float2 ps = __ldg(p.psi + k), rh = __ldg(p.rho + k);
