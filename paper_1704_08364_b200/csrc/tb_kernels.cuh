@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
         if (i < RPT / 2 && active && idx < p.n_t) {
           a = r0[idx];
           if (has1) b = r1[idx];
-          bad |= !isfinite(a) || !isfinite(b);
           if constexpr (NORM) {
             if (w.normtab) {
               const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
@@ -198,7 +197,6 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
         if (i < RPT / 2 && active && idx < p.n_t) {
           a = __ldg(y0 + idx);
           if (has1) b = __ldg(y1 + idx);
-          bad |= !isfinite(a) || !isfinite(b);
           if constexpr (NORM) {
             if (w.normtab) {
               const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
@@ -258,6 +256,11 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
     __syncthreads();
     const float2 z0 = buf[0];
     const float a0 = z0.x * p.inv_nt, a1 = z0.y * p.inv_nt;
+    // a non-finite sample anywhere in the pair reaches the DC bin through the
+    // ramp / window / FFT chain (x * 0 and inf - inf are NaN; the count
+    // normalisation propagates NaN), so the rect coefficients carry the
+    // input finiteness check (one test per pair instead of one per sample)
+    bad |= !(isfinite(a0) && isfinite(a1));
     float2* out0 = w.polar + ((size_t)q * p.prow + j0) * H;
     float2* out1 = out0 + H;
     // half turn: row V holds conj(row 0), the angle-pi mirror (fourier_bp.py:310)
