@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
   float* stage = sacc + ((p.S + 3) & ~3);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage + 4 * p.n_t);
   const int t = threadIdx.x;
-  const bool active = t < TPF;
+  // blocks are exactly TPF threads once TPF >= 32: compile-time true there
+  const bool active = TPF >= 32 || t < TPF;
   const int q = blockIdx.y;
   const int g = blockIdx.x;
   const int npairs = (p.rows + 1) >> 1;
@@ -314,7 +315,8 @@ __global__ void __launch_bounds__(KShape<NP>::THREADS) kr_ramp(DevPlan p, const 
   constexpr int RPT = K::RPT, TPF = K::TPF;
   extern __shared__ float2 smem[];
   const int t = threadIdx.x;
-  const bool active = t < TPF;
+  // blocks are exactly TPF threads once TPF >= 32: compile-time true there
+  const bool active = TPF >= 32 || t < TPF;
   const int j0 = 2 * blockIdx.x, j1 = j0 + 1;
   const bool has1 = j1 < total_rows;
   // global row index j over B slices -> (slice j / rows, row j % rows)
@@ -380,7 +382,7 @@ __device__ __forceinline__ void k1b_slice(const DevPlan& p, const Work& w, int q
   float* red = bm + p.S;  // [2 * blockDim]
   float* buf2 = red + 2 * blockDim.x;  // [H] real part of the common row
   const int t = threadIdx.x;
-  const bool active = t < TPF;
+  const bool active = t < TPF;  // launched with K1B_THREADS >= TPF threads
   const float* part = w.part + (size_t)q * w.groups * p.S;
   __syncthreads();  // smem of the previous item released
   {
@@ -825,7 +827,7 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_colu
   const int c1 = min(H + 1, c0 + cols_per_cta);
   for (int base = c0; base < c1; base += K2::G) {
     const int a = base + g;
-    const bool valid = a < c1;
+    const bool valid = K2::G == 1 || a < c1;  // one column per step: always valid
     k2_column<L, CROP_HALF>(p, w, valid ? a : c1 - 1, q, t, valid, buf);
     __syncthreads();  // buffer reuse by the next column
   }
@@ -846,7 +848,8 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
   constexpr int RPT = K::RPT, TPF = K::TPF;
   constexpr int H = L / 2;
   const int t = threadIdx.x;
-  const bool active = t < TPF;
+  // blocks are exactly TPF threads once TPF >= 32: compile-time true there
+  const bool active = TPF >= 32 || t < TPF;
   const int n = p.n;
   const float2* G = w.columns + (size_t)q * p.col_slice + (size_t)tile * (H + 1) * 4;
   const float cm = __ldcg(w.coefmean + q);  // written by another CTA (K1b)
@@ -857,8 +860,9 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
   const float xt = fmaf((float)t, inv_n, 0.5f * inv_n - 1.f);  // x of column t (+ i TPF inv_n)
   for (int pair = 0; pair < 2; ++pair) {
     const int m2a = 4 * tile + 2 * pair, m2b = m2a + 1;
-    if (m2a >= n) break;  // uniform across the CTA
-    const bool hasb = m2b < n;
+    // n = L/2 (CROP_HALF) is a multiple of 4: every tile holds 4 rows
+    if (!CROP_HALF && m2a >= n) break;  // uniform across the CTA
+    const bool hasb = CROP_HALF || m2b < n;
     float2 v[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
