@@ -75,6 +75,11 @@ struct Work {
   cudaTextureObject_t polar_tex;
 };
 
+#ifndef TB_K1_SLOTS
+#define TB_K1_SLOTS 1  // K1 TMA staging slots (row pairs)
+#endif
+#define K1_STAGE_ROWS (2 * TB_K1_SLOTS)
+
 template <int L>
 struct KShape {
   using S = FftShape<L>;
@@ -112,9 +117,12 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
   extern __shared__ float2 smem[];
   float2* buf = smem;
   float* sacc = reinterpret_cast<float*>(smem + K::BUF);
-  // two staging slots for the next row pair (TMA bulk copies), 16-B aligned
+  // staging for the row pair (TMA bulk copies), 16-B aligned: one slot,
+  // refilled with the next pair as soon as every thread holds its samples
+  // (the copy then hides behind three FFTs; a second slot would cost 16 KB
+  // of L1 per CTA)
   float* stage = sacc + ((p.S + 3) & ~3);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + 4 * p.n_t);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + K1_STAGE_ROWS * p.n_t);
   const int t = threadIdx.x;
   // blocks are exactly TPF threads once TPF >= 32: compile-time true there
   const bool active = TPF >= 32 || t < TPF;
@@ -156,12 +164,14 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
   for (int pr = pr_begin; pr < pr_end; ++pr) {
     const int j0 = 2 * pr, j1 = 2 * pr + 1;
     const bool has1 = j1 < p.rows;
-    const int slot = (pr - pr_begin) & 1;
+    const int slot = TB_K1_SLOTS == 2 ? (pr - pr_begin) & 1 : 0;
     float2 v[RPT];
     if (bulk) {
+#if TB_K1_SLOTS == 2
       // prefetch the next pair into the other slot (freed by the barrier that
       // closed the previous iteration), then wait for this pair's rows
       if (t == 0 && pr + 1 < pr_end) issue(pr + 1, slot ^ 1);
+#endif
       mbar_wait(&bars[slot], phase[slot]);
       phase[slot] ^= 1u;
       const float* r0 = stage + slot * 2 * p.n_t;
@@ -186,6 +196,10 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
         }
         v[i] = make_float2(a, b);
       }
+#if TB_K1_SLOTS == 1
+      __syncthreads();  // every thread holds its samples: the slot is free
+      if (t == 0 && pr + 1 < pr_end) issue(pr + 1, 0);
+#endif
     } else {
       const float* y0 = slice + (size_t)j0 * w.in_row;
       const float* y1 = y0 + w.in_row;

@@ -61,8 +61,9 @@ template <int L>
 struct Launch {
   using K = tb::KShape<L>;
   static size_t smem_k1(const tb_plan* p) {
-    // FFT buffer + support sums + two TMA staging slots of a row pair + 2 mbarriers
-    return K::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 + (size_t)4 * p->n_t * 4 + 16;
+    // FFT buffer + support sums + TB_K1_SLOTS TMA staging slots of a row pair + 2 mbarriers
+    return K::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 +
+           (size_t)K1_STAGE_ROWS * p->n_t * 4 + 16;
   }
   static size_t smem_k1b(const tb_plan* p) {
     return K::BUF * sizeof(float2) + (size_t)2 * std::max(p->S, 1) * 4 + (size_t)2 * K::K1B_THREADS * 4 +
