@@ -329,6 +329,23 @@ def run_ours(args):
         except CenteringError as exc:  # a slab outside the phantom has no centre to find
             pre_path = {"skipped": f"CenteringError on this rank's slab: {exc}"}
 
+    # the forward projector (K6, fp64 rays) on a one-slice
+    # sample of this rank's reconstructions, back onto the n x n sinogram grid
+    fwd = None
+    if not args.no_ss and S > 0:
+        one = torch.empty((1, n, n), dtype=torch.float32, device=dev)
+        nat.forward(img[:1], one, 1, 0.5, False, stream)  # warm-up
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        nat.forward(img[:1], one, 1, 0.5, False, stream)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1)
+        fwd = {"kernel": "k6_forward (projector.forward_project, step 0.5, bilinear)", "slices_sampled": 1,
+               "ms_per_slice": fms, "ray_samples_per_s": n * n * math.ceil(2 * math.sqrt(2) * n) / (fms / 1e3)}
+        del one
+
     # BASELINE configs[4]: the brute-force O(N^3) slant-stack backprojection
     # (fbp kernel "ss", projector.py:126-158) on the same inputs, timed on a
     # bounded sample of this rank's slices (device-resident, CUDA events)
@@ -397,6 +414,7 @@ def run_ours(args):
             "stage_ms_per_step": {k: v for k, v in stage.items() if v > 0},
             "gpu_launches": sum(launches.values()) * args.steps,
             "ss_comparator": ss,
+            "forward_projector": fwd,
             "counts_path": counts_path,
             "preprocess_path": pre_path,
             "e2e": e2e,
