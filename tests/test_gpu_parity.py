@@ -215,3 +215,28 @@ def test_determinism_repeat_bitwise():
     x = phantom.ellipsoid_volume(4, 512, 512, device="cuda")
     plan = F.BstPlan(512, 512)
     assert torch.equal(F.fbp_volume(x, plan), F.fbp_volume(x, plan))
+
+
+def test_largest_radial_length_8192_properties():
+    """L = 8192 (n_t = 4096, 512-thread FFT blocks, remainder-free radix-16 x 3
+    + radix-2): linearity, the constant-sinogram identity (c * coverage) and
+    batch invariance, without a CPU oracle at this size."""
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    n_t, v = 4096, 256
+    plan = F.BstPlan(n_t, v)
+    assert plan.radial_samples == 8192
+    x = phantom.ellipsoid_volume(2, n_t, v, device="cuda")
+    g = torch.Generator("cuda").manual_seed(4)
+    z = torch.randn(x.shape, device="cuda", generator=g)
+    fx = F.fbp_volume(x, plan)
+    fz = F.fbp_volume(z, plan)
+    fxz = F.fbp_volume(2.0 * x - 0.5 * z, plan)
+    lin = torch.linalg.norm(fxz - (2.0 * fx - 0.5 * fz)) / torch.linalg.norm(fxz)
+    assert lin.item() < 1e-5
+    one = F.fbp_volume(x[1:2].contiguous(), plan, batch=1)
+    assert torch.equal(one[0], fx[1])
+    const = torch.full((1, v, n_t), 0.5, device="cuda")
+    b = F.fbp_volume(const, plan, kernel="none")[0].cpu().numpy()
+    expect = 0.5 * O.OraclePlan(n_t, v).coverage()
+    assert np.max(np.abs(b - expect)) <= 1e-4 * np.pi * 0.5
