@@ -563,7 +563,9 @@ def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, c
     if not sino.is_pinned():
         sino = sino.pin_memory()
     if chunk is None:
-        chunk = max(batch, 16 if plan.radial_samples >= 4096 else 64)
+        # ~128 MiB of sinogram per copy: PCIe (not the kernels) bounds this
+        # path, so small chunks shrink the un-overlapped first H2D / last D2H
+        chunk = max(1, min(64, (128 << 20) // max(1, A * n_t * 4)))
     slabs = _split(S, len(devices))
     states = []
     for dev, (b, e) in zip(devices, slabs):
