@@ -193,6 +193,38 @@ class ClockSampler:
 # our implementation
 # ---------------------------------------------------------------------------
 
+def _transfer_lines(torch, host_in, host_out, dev, bytes_per_dir, e2e_s):
+    """H2D alone, D2H alone and both at once (pinned, 256 MiB copies, 4 GiB
+    per direction) on the e2e buffers: the PCIe floor the e2e number sits on."""
+    chunk = 64 << 20  # floats = 256 MiB
+    nchunk = 16
+    hi, ho = host_in.view(-1), host_out.view(-1)
+    nchunk = min(nchunk, hi.numel() // chunk)
+    dbuf = torch.empty(2 * chunk, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def run(h2d, d2h):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(nchunk):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    dbuf[:chunk].copy_(hi[i * chunk:(i + 1) * chunk], non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    ho[i * chunk:(i + 1) * chunk].copy_(dbuf[chunk:], non_blocking=True)
+        torch.cuda.synchronize()
+        return nchunk * chunk * 4 / (time.perf_counter() - t0) / 1e9
+
+    if nchunk == 0:
+        return None
+    run(True, True)
+    h2d, d2h, both = run(True, False), run(False, True), run(True, True)
+    floor = bytes_per_dir / (both * 1e9)
+    return {"h2d_GBps": h2d, "d2h_GBps": d2h, "concurrent_GBps_per_direction": both,
+            "pcie_floor_s": floor, "e2e_frac_of_pcie_floor": floor / e2e_s}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -225,7 +257,11 @@ def run_ours(args):
     # synthetic input: per-slice analytic ellipsoid sinogram of this rank's slab
     sino = phantom.ellipsoid_volume(n, n, n, device=dev, chunk=32, slices=(b, e))
     img = torch.empty((S, n, n), dtype=torch.float32, device=dev)
-    nat = F.native_plan(plan, F.FilterPlan(), False, local)
+    torch.cuda.synchronize()
+    tp = time.perf_counter()
+    nat = F.native_plan(plan, F.FilterPlan(), False, local)  # host tables + device gridding table
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - tp) * 1e3
     ws = nat.new_workspace(batch)
     stream = torch.cuda.current_stream(dev)
 
@@ -384,6 +420,7 @@ def run_ours(args):
         e2e_s = max_over_ranks((time.perf_counter() - t0) / k)
         e2e = {"value": (n ** 3) / e2e_s, "unit": UNIT, "s_per_step": e2e_s,
                "h2d_bytes_per_step": S * n * n * 4, "d2h_bytes_per_step": S * n * n * 4}
+        e2e["transfers"] = _transfer_lines(torch, host_in, host_out, dev, S * n * n * 4, e2e_s)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -418,6 +455,7 @@ def run_ours(args):
             "counts_path": counts_path,
             "preprocess_path": pre_path,
             "e2e": e2e,
+            "plan_create_ms": plan_ms,
             "cpu_baseline": cpu,
             "clocks": clk,
         }
