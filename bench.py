@@ -236,17 +236,25 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TB_BENCH_BACKEND=gloo: ranks may share a GPU (exercises the multi-rank
+    # path on one device; the timing reductions then run on host tensors)
+    backend = os.environ.get("TB_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def max_over_ranks(x):
-        return slabs.max_over_ranks(x, device=dev)
+        return slabs.max_over_ranks(x, device=dev if backend == "nccl" else None)
 
     n = args.size
     plan = F.BstPlan(n, n)
@@ -419,7 +427,8 @@ def run_ours(args):
         barrier()
         e2e_s = max_over_ranks((time.perf_counter() - t0) / k)
         e2e = {"value": (n ** 3) / e2e_s, "unit": UNIT, "s_per_step": e2e_s,
-               "h2d_bytes_per_step": S * n * n * 4, "d2h_bytes_per_step": S * n * n * 4}
+               "h2d_bytes_per_step": n ** 3 * 4, "d2h_bytes_per_step": n ** 3 * 4,
+               "bytes_per_rank_per_direction": S * n * n * 4}
         e2e["transfers"] = _transfer_lines(torch, host_in, host_out, dev, S * n * n * 4, e2e_s)
 
     cpu = None
@@ -434,7 +443,7 @@ def run_ours(args):
     if rank == 0:
         cfg = _workload(n)
         cfg.update({"batch": batch, "slab_slices_per_rank": S, "parallelism": f"slab{world}",
-                    "l2": "inputs larger than L2 (32 GiB sinogram volume streamed per step)"})
+                    "l2": f"inputs larger than L2 ({S * n * n * 4 / 2**30:g} GiB sinogram slab streamed per step per rank)"})
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "seconds_per_volume": ms_step / 1e3,
