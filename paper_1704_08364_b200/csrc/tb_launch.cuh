@@ -94,6 +94,18 @@ struct Launch {
     }
     TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    // tuning: shared-memory carveout (percent of the SM's 228 KB; the rest is
+    // L1) for K1 / K2 / K3 as "k1,k2,k3"; unset = the driver's choice
+    if (const char* e = std::getenv("TB_CARVEOUT")) {
+      int c1 = -1, c2 = -1, c3 = -1;
+      if (std::sscanf(e, "%d,%d,%d", &c1, &c2, &c3) == 3) {
+        const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
+        TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, co, c1));
+        TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, co, c1));
+        TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, (L >= 64)>, co, c2));
+        TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, (L >= 64)>, co, c3));
+      }
+    }
     return TB_OK;
   }
 
