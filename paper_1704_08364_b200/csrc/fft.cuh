@@ -198,10 +198,23 @@ struct FftShape {
   __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
 };
 
+// Barrier policies for the passes: the whole CTA, or one named barrier per
+// group of threads that owns its own transform (several independent
+// transforms in one CTA, decoupled from each other).
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct GroupSync {
+  int id, count;  // bar.sync id (1..15; 0 is __syncthreads), threads in the group
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
+};
+
 // One Stockham pass.  tw[j] = exp(-2 pi i j / N) for j < N (fp32).
-template <int N, int PASS, bool INV>
+template <int N, int PASS, bool INV, class Sync = CtaSync>
 __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
-                                         const float2* __restrict__ tw) {
+                                         const float2* __restrict__ tw, Sync sync = Sync()) {
   using S = FftShape<N>;
   constexpr int R = S::radix(PASS);
   constexpr int NS = S::ns(PASS);
@@ -226,7 +239,7 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
         x[b][m] = active ? buf[spad(t + b * S::TPF + m * NB)] : make_float2(0.f, 0.f);
       }
     }
-  if constexpr (!FIRST) __syncthreads();
+  if constexpr (!FIRST) sync();
 #pragma unroll
   for (int b = 0; b < PER; ++b) {
     const int j = t + b * S::TPF;
@@ -272,28 +285,28 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
       }
     }
   }
-  if constexpr (!LAST) __syncthreads();
+  if constexpr (!LAST) sync();
 }
 
-template <int N, bool INV, int PASS = 0>
+template <int N, bool INV, int PASS = 0, class Sync = CtaSync>
 __device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
-                                           const float2* __restrict__ tw) {
+                                           const float2* __restrict__ tw, Sync sync = Sync()) {
   if constexpr (PASS < FftShape<N>::NPASS) {
     // every thread runs the same instruction stream (bar.sync is .aligned:
     // no barrier may sit under a thread-divergent branch); idle threads only
     // mask their shared-memory and table traffic
-    fft_pass<N, PASS, INV>(v, buf, t, active, tw);
-    fft_passes<N, INV, PASS + 1>(v, buf, t, active, tw);
+    fft_pass<N, PASS, INV, Sync>(v, buf, t, active, tw, sync);
+    fft_passes<N, INV, PASS + 1, Sync>(v, buf, t, active, tw, sync);
   }
 }
 
 // Full transform.  Must be called by every thread of the CTA (barriers);
 // threads with !active compute on zeros and touch no memory.  On return the
 // buffer may be reused only after a __syncthreads().
-template <int N, bool INV>
+template <int N, bool INV, class Sync = CtaSync>
 __device__ __forceinline__ void fft(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
-                                    const float2* __restrict__ tw) {
-  fft_passes<N, INV, 0>(v, buf, t, active, tw);
+                                    const float2* __restrict__ tw, Sync sync = Sync()) {
+  fft_passes<N, INV, 0, Sync>(v, buf, t, active, tw, sync);
 }
 
 }  // namespace tb

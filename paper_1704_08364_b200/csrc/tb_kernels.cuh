@@ -643,9 +643,9 @@ __device__ __forceinline__ uint2 ld_table(const uint2* p) {
 // of thread t at smem[i * TPF + t]) so they leave registers during the
 // latency-bound gather; a barrier separates the reload from the first FFT
 // pass, which rewrites the buffer.
-template <int L, bool CROP_HALF>
+template <int L, bool CROP_HALF, class Sync>
 __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a, int q, int t, bool active,
-                                          float2* smem) {
+                                          float2* smem, Sync sync) {
   float2* stg = smem;
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
@@ -852,7 +852,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     }
 #pragma unroll
     for (int i = 0; i < RPT; ++i) v[i] = active ? stg[i * TPF + t] : make_float2(0.f, 0.f);
-    __syncthreads();  // every thread holds its nodes before the FFT rewrites the buffer
+    sync();  // every thread holds its nodes before the FFT rewrites the buffer
   } else {
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -872,7 +872,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       v[i] = val;
     }
   }
-  fft<L, true>(v, smem, t, active, p.tw_L);
+  fft<L, true, Sync>(v, smem, t, active, p.tw_L, sync);
   if (active) {
     float2* out = w.columns + (size_t)q * p.col_slice;
 #pragma unroll
@@ -901,6 +901,9 @@ struct K2Shape {
 #ifndef TB_K2_MINB
 #define TB_K2_MINB 3
 #endif
+#ifndef TB_K2_NAMED
+#define TB_K2_NAMED 1
+#endif
   static constexpr int MINB = THREADS <= 256 ? TB_K2_MINB : 1;
   static constexpr int SMEM_PER_GROUP = KShape<L>::BUF;  // float2 FFT buffer (+ gather staging)
 };
@@ -917,11 +920,28 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_colu
   const int q = blockIdx.y;
   const int c0 = blockIdx.x * cols_per_cta;
   const int c1 = min(H + 1, c0 + cols_per_cta);
-  for (int base = c0; base < c1; base += K2::G) {
-    const int a = base + g;
-    const bool valid = K2::G == 1 || a < c1;  // one column per step: always valid
-    k2_column<L, CROP_HALF>(p, w, valid ? a : c1 - 1, q, t, valid, buf);
-    __syncthreads();  // buffer reuse by the next column
+  if constexpr (K2::G == 1) {
+    for (int a = c0; a < c1; ++a) {
+      k2_column<L, CROP_HALF>(p, w, a, q, t, true, buf, CtaSync());
+      __syncthreads();  // buffer reuse by the next column
+    }
+  } else if constexpr (TPF % 32 == 0 && K2::G < 16 && TB_K2_NAMED) {
+    // G column groups side by side on one SM (adjacent columns at the same
+    // time share their polar lines in L1), each synchronising only itself
+    // through its own named barrier: no coupling between the groups
+    const GroupSync gs{1 + g, TPF};
+    for (int a = c0 + g; a < c1; a += K2::G) {
+      k2_column<L, CROP_HALF>(p, w, a, q, t, true, buf, gs);
+      gs();  // buffer reuse by the next column
+    }
+  } else {
+    // sub-warp groups (small L): CTA-wide barriers, idle groups on the tail
+    for (int base = c0; base < c1; base += K2::G) {
+      const int a = base + g;
+      const bool valid = a < c1;
+      k2_column<L, CROP_HALF>(p, w, valid ? a : c1 - 1, q, t, valid, buf, CtaSync());
+      __syncthreads();  // buffer reuse by the next column
+    }
   }
 }
 
