@@ -686,20 +686,21 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     constexpr int NP = TB_K2_NP < RPT ? TB_K2_NP : RPT, NG = RPT / NP, AH = TB_K2_AHEAD;
     uint2 e[RPT];
     float4 fre[RPT], fim[RPT];
+    // t < TPF: node b = t + i TPF lies in the lower half plane (b >= H,
+    // signed b < 0) exactly when i >= RPT/2 -- a compile-time split; there
+    // the table row is read at L - b (= H for b = H, the same entry)
     auto tload = [&](int i) {
       const int b = t + i * TPF;
-      const int ab = b <= H ? b : L - b;
+      const int ab = i < RPT / 2 ? b : L - b;
       e[i] = active ? ld_table(trow + ab) : make_uint2(0xFFFFu, 0u);
     };
     auto fetch = [&](int i) {
-      const int b = t + i * TPF;
-      const int bs = b < H ? b : b - L;
       const uint2 ej = e[i];
       const int r0 = (int)(ej.x & 0xFFFFu);
       const int ra = r0 == 0xFFFF ? 0 : r0;
       const int I = (int)(ej.x >> 16);
       const int qt = (int)(ej.y >> 16);
-      const bool flip = (as < 0) != (bs < 0);
+      const bool flip = (as < 0) != (i >= RPT / 2);
       const int t0 = flip ? (qt ? V - I - 1 : V - I) : I;
       fre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       fim[i] = fre[i];
@@ -710,13 +711,11 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       }
     };
     auto consume = [&](int i) {
-      const int b = t + i * TPF;
-      const int bs = b < H ? b : b - L;
       const uint2 ej = e[i];
       const int r0 = (int)(ej.x & 0xFFFFu);
       const int ra = r0 == 0xFFFF ? 0 : r0;
       int qt = (int)(ej.y >> 16);
-      const bool flip = (as < 0) != (bs < 0);
+      const bool flip = (as < 0) != (i >= RPT / 2);
       if (flip) qt = qt ? 65536 - qt : 0;
       const float r = (float)(ej.y & 0xFFFFu) * (1.f / 65536.f), u = (float)qt * (1.f / 65536.f);
       const float4 re = fre[i], im = fim[i];
@@ -727,7 +726,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       const float2 r1v = make_float2(fmaf(r, p11.x - p10.x, p10.x), fmaf(r, p11.y - p10.y, p10.y));
       float2 val = make_float2(fmaf(u, r1v.x - r0v.x, r0v.x) + fmaf(r, cc.y - cc.x, cc.x),
                                fmaf(u, r1v.y - r0v.y, r0v.y));
-      if (b >= H) val.y = -val.y;
+      if (i >= RPT / 2) val.y = -val.y;
       if (p.has_mod) val = cmul(val, cmul(m_t, __ldg(p.modt + i * TPF)));
       if (active) stg[i * TPF + t] = r0 == 0xFFFF ? make_float2(0.f, 0.f) : val;
     };
