@@ -948,6 +948,23 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_colu
 // K3: C2R along k1 for a tile of 4 output rows (two packed pairs) + epilogue
 // ---------------------------------------------------------------------------
 
+// atan(s) for s in [0, 1] (s <= 1: pixel centres satisfy r^2 < 2): s P(s^2)
+// with a degree-8 least-max-error fit, 1.1e-7 max abs error in fp32 (as good
+// as asinf; 9 FMAs instead of asinf's branches and square root)
+__device__ __forceinline__ float atan01(float s) {
+  const float z = s * s;
+  float q = 0.0024567015934735537f;
+  q = fmaf(q, z, -0.014401277527213097f);
+  q = fmaf(q, z, 0.0397811196744442f);
+  q = fmaf(q, z, -0.07234852015972137f);
+  q = fmaf(q, z, 0.10498946160078049f);
+  q = fmaf(q, z, -0.14161230623722076f);
+  q = fmaf(q, z, 0.19985906779766083f);
+  q = fmaf(q, z, -0.33332598209381104f);
+  q = fmaf(q, z, 0.9999998807907104f);
+  return s * q;
+}
+
 // One 4-row output tile (two packed row pairs) of the slice in workspace
 // slot q, written to img_slice [n][n].  The K2 columns
 // already carry the full half-node modulation M[a] M[b].  `chk` accumulates
@@ -968,6 +985,7 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
   const float A = p.img_scale * out_scale;       // amplitude / L^2 / (2 pi)
   const float cmo = cm * out_scale;               // coef_mean / (2 pi)
   const float Bpi = cmo * 3.14159265358979323846f;  // inside the unit circle
+  const float cm2 = -2.f * cmo;
   const float xt = fmaf((float)t, inv_n, 0.5f * inv_n - 1.f);  // x of column t (+ i TPF inv_n)
   for (int pair = 0; pair < 2; ++pair) {
     const int m2a = 4 * tile + 2 * pair, m2b = m2a + 1;
@@ -1019,8 +1037,9 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
           float ra = fmaf(v[i].x, A, Bpi);
           float rb = fmaf(v[i].y, A, Bpi);
           const float r2a = fmaf(x1, x1, x2a * x2a), r2b = fmaf(x1, x1, x2b * x2b);
-          if (r2a > 1.f) ra += cmo * (2.f * asinf(rsqrtf(r2a)) - 3.14159265358979323846f);
-          if (r2b > 1.f) rb += cmo * (2.f * asinf(rsqrtf(r2b)) - 3.14159265358979323846f);
+          // outside the unit circle 2 asin(1/r) - pi = -2 atan(sqrt(r^2 - 1))
+          if (r2a > 1.f) { const float d = r2a - 1.f; ra = fmaf(cm2, atan01(d * rsqrtf(d)), ra); }
+          if (r2b > 1.f) { const float d = r2b - 1.f; rb = fmaf(cm2, atan01(d * rsqrtf(d)), rb); }
           oa[m1] = ra;
           chk = fmaf(ra, 0.f, chk);
           if (hasb) {
