@@ -77,7 +77,11 @@ struct Launch {
     if (const char* e = std::getenv("TB_K2_COLS"))  // tuning: columns swept per CTA
       if (std::atoi(e) > 0) return K2::G * std::atoi(e);
     const int resident = K2::MINB;  // CTAs per SM
-    const int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
+    int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
+    // L = 4096: the resident CTAs should cover a little less than one slice,
+    // so the slice's polar spectrum and the gridding table stay in L2
+    // (measured at 2048^3: 4 columns per CTA 101.9 ms, 5 columns 103.3 ms)
+    if (L == 4096 && steps > 1) steps -= 1;
     return K2::G * std::max(1, steps);
   }
 
