@@ -137,6 +137,9 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
   const bool bulk = (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0) && (w.in_row & 3) == 0 &&
                     (w.in_slice & 3) == 0;
   auto issue = [&](int pr, int slot) {
+    // the slot was last read by generic-proxy loads (ordered before this
+    // thread by the barrier); order them before the async-proxy refill
+    fence_proxy_async_smem();
     const int j0 = 2 * pr;
     const int nrow = (2 * pr + 1 < p.rows) ? 2 : 1;
     const uint32_t bytes = (uint32_t)(nrow * p.n_t * 4);
