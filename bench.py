@@ -286,15 +286,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one event between consecutive steps as well (per-step median, SURVEY
+    # §8d); recording an event does not perturb the stream
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
     ev0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         step()
+        if i < args.steps - 1:
+            marks[i].record(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms_total / args.steps
+    bounds = [ev0] + marks + [ev1]
+    per_step = [max_over_ranks(bounds[i].elapsed_time(bounds[i + 1])) for i in range(args.steps)]
+    step_stats = {"median": statistics.median(per_step), "min": min(per_step), "max": max(per_step)}
     value = (n ** 3) / (ms_step / 1e3)
 
     # per-kernel device times on the same workload (one extra profiled step)
@@ -447,6 +455,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "seconds_per_volume": ms_step / 1e3,
+            "ms_per_step_stats": step_stats,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (analytic off-centre ellipsoid sinograms, generated on device)",
             "config": cfg,
