@@ -387,6 +387,8 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   // --- K1 work split: <= 256 CTAs (partial-sum groups) per slice
   const int npairs = (p->rows + 1) / 2;
   p->pairs_per_cta = std::max(1, (npairs + 255) / 256);
+  if (const char* e = std::getenv("TB_K1_PAIRS"))  // tuning: row pairs per K1 CTA
+    if (std::atoi(e) > 0) p->pairs_per_cta = std::atoi(e);
   p->groups = (npairs + p->pairs_per_cta - 1) / p->pairs_per_cta;
 
   // --- host tables
