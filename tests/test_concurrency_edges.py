@@ -68,3 +68,18 @@ def test_single_slice_api_equals_volume_slice():
     y = Sinogram(DetectorAxis(128), AngleAxis(128), vol[1].cpu().numpy().astype(np.float64))
     img = F.fbp(y, plan)
     assert np.array_equal(np.asarray(img.data, dtype=np.float32), v[1].cpu().numpy())
+
+
+def test_plain_gather_path_matches_texture_path():
+    """A launch group whose polar rows exceed the pitch-2D texture height
+    (batch * (n_theta + 1) > 65000) gathers with plain loads instead of TLD4;
+    both paths compute the same bilinear weights on the same fp32 texels."""
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    plan = F.BstPlan(64, 2048)
+    vol = phantom.ellipsoid_volume(40, 64, 2048, device="cuda")
+    vol += 0.01 * torch.randn(vol.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    tex = F.fbp_volume(vol, plan, batch=1)     # 2049 rows: texture gathers
+    plain = F.fbp_volume(vol, plan, batch=40)  # 81960 rows: plain loads
+    rel = (torch.linalg.norm(tex - plain) / torch.linalg.norm(tex)).item()
+    assert rel < 1e-6, rel
