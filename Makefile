@@ -26,6 +26,14 @@ $(LIB): $(OBJ)/tb_api.o $(INST)
 	@mkdir -p $(PKG)/lib
 	$(NVCC) $(ARCH) -shared -o $@ $^
 
+# C99 client of the ABI (no Python): tests/c/abi_smoke.c
+C_SMOKE := $(OBJ)/c_abi_smoke
+c_smoke: $(C_SMOKE)
+$(C_SMOKE): tests/c/abi_smoke.c include/tb_bst.h $(LIB)
+	@mkdir -p $(OBJ)
+	gcc -std=c99 -O2 -Wall -Wextra -D_DEFAULT_SOURCE -Iinclude -I/usr/local/cuda/include $< -o $@ \
+	  -L$(PKG)/lib -ltb_bst -Wl,-rpath,'$$ORIGIN/../lib' -L/usr/local/cuda/lib64 -lcudart -lm
+
 # registers / spills of the L = 4096 kernels
 ptxas: $(CSRC)/tb_inst.cu $(HDR)
 	$(NVCC) $(NVFLAGS) -DTB_L=4096 -Xptxas -v -c -o /tmp/tb_inst_4096.o $< 2>&1 | grep -E "Compiling|registers|spill"
@@ -36,4 +44,4 @@ sass: $(LIB)
 clean:
 	rm -rf $(LIB) $(OBJ)
 
-.PHONY: all clean ptxas sass
+.PHONY: all clean ptxas sass c_smoke
