@@ -76,7 +76,11 @@ struct Work {
 };
 
 #ifndef TB_K1_SLOTS
-#define TB_K1_SLOTS 1  // K1 TMA staging slots (row pairs)
+// K1 TMA staging slots (row pairs).  0 = coalesced direct row loads: the
+// measured default (2048^3 equal within noise, 1024^3 -1.6 %, 512^3 -2 %):
+// the 16 KB staging slot cost more in L1 / co-residency with the other
+// lane than the latency it hid
+#define TB_K1_SLOTS 0
 #endif
 #define K1_STAGE_ROWS (2 * TB_K1_SLOTS)
 
@@ -110,17 +114,20 @@ __device__ __forceinline__ float norm_line(float I, float2 nt, float eps) {
 // ---------------------------------------------------------------------------
 // K1: radial kernel (fused ramp when npad == L; fused normalisation when NORM)
 // ---------------------------------------------------------------------------
+#ifndef TB_K1_MINB
+#define TB_K1_MINB TB_MINB
+#endif
 template <int L, bool RAMP, bool NORM>
-__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_K1_MINB : 1)
+    k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
   extern __shared__ float2 smem[];
   float2* buf = smem;
   float* sacc = reinterpret_cast<float*>(smem + K::BUF);
-  // staging for the row pair (TMA bulk copies), 16-B aligned: one slot,
-  // refilled with the next pair as soon as every thread holds its samples
-  // (the copy then hides behind three FFTs; a second slot would cost 16 KB
-  // of L1 per CTA)
+  // staging for the row pair (TMA bulk copies, TB_K1_SLOTS > 0), 16-B
+  // aligned: one slot, refilled with the next pair as soon as every thread
+  // holds its samples (the copy then hides behind three FFTs)
   float* stage = sacc + ((p.S + 3) & ~3);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage + K1_STAGE_ROWS * p.n_t);
   const int t = threadIdx.x;
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k1_radial
   const int H = L / 2;
   const float* slice = sino + (size_t)q * w.in_slice;
   // bulk copies need 16-byte aligned rows; otherwise read rows directly
-  const bool bulk = (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0) && (w.in_row & 3) == 0 &&
+  const bool bulk = TB_K1_SLOTS > 0 && (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0) && (w.in_row & 3) == 0 &&
                     (w.in_slice & 3) == 0;
   auto issue = [&](int pr, int slot) {
     // the slot was last read by generic-proxy loads (ordered before this
