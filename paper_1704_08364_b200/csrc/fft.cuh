@@ -189,17 +189,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-template <int N>
+__host__ __device__ constexpr int default_rpt(int n) { return n < 16 ? n : 16; }
+
+// RPT_ points per thread (a power of two <= 16; default 16): full radix-RPT_
+// passes, then one remainder pass
+template <int N, int RPT_ = default_rpt(N)>
 struct FftShape {
   static_assert((N & (N - 1)) == 0 && N >= 2, "power of two");
-  static constexpr int RPT = N < 16 ? N : 16;  // points per thread
+  static_assert((RPT_ & (RPT_ - 1)) == 0 && RPT_ >= 2 && RPT_ <= 16 && RPT_ <= N, "points per thread");
+  static constexpr int RPT = RPT_;             // points per thread
   static constexpr int TPF = N / RPT;          // threads per transform
   static constexpr int P = ilog2(N);
-  static constexpr int N16 = N >= 16 ? P / 4 : 0;                   // radix-16 passes
-  static constexpr int REM = N >= 16 ? (1 << (P % 4)) : N;          // remainder radix (last)
-  static constexpr int NPASS = N >= 16 ? N16 + (REM > 1 ? 1 : 0) : 1;
+  static constexpr int LR = ilog2(RPT);
+  static constexpr int NFULL = P / LR;                              // radix-RPT passes
+  static constexpr int REM = 1 << (P % LR);                         // remainder radix (last)
+  static constexpr int NPASS = NFULL + (REM > 1 ? 1 : 0);
   static constexpr int SMEM = NPASS > 1 ? N + N / 16 : 0;          // float2 elements
-  __host__ __device__ static constexpr int radix(int p) { return N < 16 ? N : (p < N16 ? 16 : REM); }
+  __host__ __device__ static constexpr int radix(int p) { return p < NFULL ? RPT : REM; }
   __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
 };
 
@@ -217,10 +223,10 @@ struct GroupSync {
 };
 
 // One Stockham pass.  tw[j] = exp(-2 pi i j / N) for j < N (fp32).
-template <int N, int PASS, bool INV, class Sync = CtaSync>
-__device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
+template <int N, int PASS, bool INV, class Sync = CtaSync, int RP = default_rpt(N)>
+__device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
                                          const float2* __restrict__ tw, Sync sync = Sync()) {
-  using S = FftShape<N>;
+  using S = FftShape<N, RP>;
   constexpr int R = S::radix(PASS);
   constexpr int NS = S::ns(PASS);
   constexpr int NB = N / R;
@@ -293,25 +299,25 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N>::RPT], float2* 
   if constexpr (!LAST) sync();
 }
 
-template <int N, bool INV, int PASS = 0, class Sync = CtaSync>
-__device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
+template <int N, bool INV, int PASS = 0, class Sync = CtaSync, int RP = default_rpt(N)>
+__device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
                                            const float2* __restrict__ tw, Sync sync = Sync()) {
-  if constexpr (PASS < FftShape<N>::NPASS) {
+  if constexpr (PASS < FftShape<N, RP>::NPASS) {
     // every thread runs the same instruction stream (bar.sync is .aligned:
     // no barrier may sit under a thread-divergent branch); idle threads only
     // mask their shared-memory and table traffic
-    fft_pass<N, PASS, INV, Sync>(v, buf, t, active, tw, sync);
-    fft_passes<N, INV, PASS + 1, Sync>(v, buf, t, active, tw, sync);
+    fft_pass<N, PASS, INV, Sync, RP>(v, buf, t, active, tw, sync);
+    fft_passes<N, INV, PASS + 1, Sync, RP>(v, buf, t, active, tw, sync);
   }
 }
 
 // Full transform.  Must be called by every thread of the CTA (barriers);
 // threads with !active compute on zeros and touch no memory.  On return the
 // buffer may be reused only after a __syncthreads().
-template <int N, bool INV, class Sync = CtaSync>
-__device__ __forceinline__ void fft(float2 (&v)[FftShape<N>::RPT], float2* buf, int t, bool active,
+template <int N, bool INV, class Sync = CtaSync, int RP = default_rpt(N)>
+__device__ __forceinline__ void fft(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
                                     const float2* __restrict__ tw, Sync sync = Sync()) {
-  fft_passes<N, INV, 0, Sync>(v, buf, t, active, tw, sync);
+  fft_passes<N, INV, 0, Sync, RP>(v, buf, t, active, tw, sync);
 }
 
 }  // namespace tb

@@ -649,6 +649,38 @@ __device__ __forceinline__ uint2 ld_table(const uint2* p) {
   return v;
 }
 
+// K2 kernel: CTA of G column groups (G*TPF = 512 threads for L <= 8192)
+// sweeping a contiguous run of columns G at a time.  Adjacent columns read
+// nearly the same polar lines, so the SM's L1 keeps the shared footprint of
+// the G concurrent columns and of the next step resident.
+#ifndef TB_K2_RPT
+#define TB_K2_RPT 16
+#endif
+template <int L>
+struct K2Shape {
+  // points per thread of the column transform (TB_K2_RPT, capped at the
+  // default for small L)
+  static constexpr int RPT = TB_K2_RPT < default_rpt(L) ? TB_K2_RPT : default_rpt(L);
+  using S = FftShape<L, RPT>;
+  static constexpr int TPF = S::TPF;
+#ifndef TB_K2_THREADS
+#define TB_K2_THREADS 256
+#endif
+  static constexpr int G = TPF >= TB_K2_THREADS ? 1 : TB_K2_THREADS / TPF;
+  static constexpr int THREADS = G * TPF;
+#ifndef TB_K2_MINB
+#define TB_K2_MINB 3
+#endif
+#ifndef TB_K2_NAMED
+#define TB_K2_NAMED 1
+#endif
+#ifndef TB_K2_MINB512
+#define TB_K2_MINB512 2
+#endif
+  static constexpr int MINB = THREADS <= 256 ? TB_K2_MINB : (THREADS <= 512 ? TB_K2_MINB512 : 1);
+  static constexpr int SMEM_PER_GROUP = KShape<L>::BUF;  // float2 FFT buffer (+ gather staging)
+};
+
 // Finished nodes are staged in the FFT buffer (thread-private slots: node i
 // of thread t at smem[i * TPF + t]) so they leave registers during the
 // latency-bound gather; a barrier separates the reload from the first FFT
@@ -657,8 +689,8 @@ template <int L, bool CROP_HALF, class Sync>
 __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a, int q, int t, bool active,
                                           float2* smem, Sync sync) {
   float2* stg = smem;
-  using K = KShape<L>;
-  constexpr int RPT = K::RPT, TPF = K::TPF;
+  using K2 = K2Shape<L>;
+  constexpr int RPT = K2::RPT, TPF = K2::TPF;
   constexpr int H = L / 2;
   const int as = a < H ? a : -H;
   const float2* pol = w.polar + (size_t)q * p.prow * H;
@@ -881,7 +913,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       v[i] = val;
     }
   }
-  fft<L, true, Sync>(v, smem, t, active, p.tw_L, sync);
+  fft<L, true, Sync, RPT>(v, smem, t, active, p.tw_L, sync);
   if (active) {
     float2* out = w.columns + (size_t)q * p.col_slice;
 #pragma unroll
@@ -894,28 +926,6 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     }
   }
 }
-
-// K2 kernel: CTA of G column groups (G*TPF = 512 threads for L <= 8192)
-// sweeping a contiguous run of columns G at a time.  Adjacent columns read
-// nearly the same polar lines, so the SM's L1 keeps the shared footprint of
-// the G concurrent columns and of the next step resident.
-template <int L>
-struct K2Shape {
-  static constexpr int TPF = FftShape<L>::TPF;
-#ifndef TB_K2_THREADS
-#define TB_K2_THREADS 256
-#endif
-  static constexpr int G = TPF >= TB_K2_THREADS ? 1 : TB_K2_THREADS / TPF;
-  static constexpr int THREADS = G * TPF;
-#ifndef TB_K2_MINB
-#define TB_K2_MINB 3
-#endif
-#ifndef TB_K2_NAMED
-#define TB_K2_NAMED 1
-#endif
-  static constexpr int MINB = THREADS <= 256 ? TB_K2_MINB : 1;
-  static constexpr int SMEM_PER_GROUP = KShape<L>::BUF;  // float2 FFT buffer (+ gather staging)
-};
 
 template <int L, bool CROP_HALF>
 __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_columns(DevPlan p, Work w, int cols_per_cta) {
