@@ -719,13 +719,20 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     // AH + 1 groups ahead, texture gathers AH groups ahead, bilinear of this
     // group (the gathers of the next groups are in flight while this one
     // computes; measured K2 -5 % against issue-then-consume groups)
-#ifndef TB_K2_NP
-#define TB_K2_NP 1
+    // measured: L = 4096 two nodes per stage one stage ahead (K2 101.8 ->
+    // 101.4 ms at 2048^3); smaller L one node per stage two ahead (the
+    // two-node form is 1-3 % slower there)
+#ifdef TB_K2_NP
+    constexpr int NP0 = TB_K2_NP;
+#else
+    constexpr int NP0 = L == 4096 ? 2 : 1;
 #endif
-#ifndef TB_K2_AHEAD
-#define TB_K2_AHEAD 2
+#ifdef TB_K2_AHEAD
+    constexpr int AH = TB_K2_AHEAD;
+#else
+    constexpr int AH = L == 4096 ? 1 : 2;
 #endif
-    constexpr int NP = TB_K2_NP < RPT ? TB_K2_NP : RPT, NG = RPT / NP, AH = TB_K2_AHEAD;
+    constexpr int NP = NP0 < RPT ? NP0 : RPT, NG = RPT / NP;
     uint2 e[RPT];
     float4 fre[RPT], fim[RPT];
     // t < TPF: node b = t + i TPF lies in the lower half plane (b >= H,
