@@ -668,16 +668,21 @@ struct K2Shape {
 #endif
   static constexpr int G = TPF >= TB_K2_THREADS ? 1 : TB_K2_THREADS / TPF;
   static constexpr int THREADS = G * TPF;
+// CTAs per SM asked of ptxas for <= 256-thread K2 CTAs: 4 (64 registers).
+// ptxas spills ~200 B per thread in the FFT phase, yet K2 drops 101.5 ->
+// 95.3 ms at 2048^3 (11.29 -> 11.15 at 1024^3, 1.46 -> 1.42 at 512^3): a
+// fourth resident column hides more gather latency than the spills cost
 #ifndef TB_K2_MINB
-#define TB_K2_MINB 3
+#define TB_K2_MINB 4
 #endif
+#define TB_K2_MINB_L(L) TB_K2_MINB
 #ifndef TB_K2_NAMED
 #define TB_K2_NAMED 1
 #endif
 #ifndef TB_K2_MINB512
 #define TB_K2_MINB512 2
 #endif
-  static constexpr int MINB = THREADS <= 256 ? TB_K2_MINB : (THREADS <= 512 ? TB_K2_MINB512 : 1);
+  static constexpr int MINB = THREADS <= 256 ? TB_K2_MINB_L(L) : (THREADS <= 512 ? TB_K2_MINB512 : 1);
   static constexpr int SMEM_PER_GROUP = KShape<L>::BUF;  // float2 FFT buffer (+ gather staging)
 };
 
