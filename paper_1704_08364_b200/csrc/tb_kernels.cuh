@@ -114,8 +114,10 @@ __device__ __forceinline__ float norm_line(float I, float2 nt, float eps) {
 // ---------------------------------------------------------------------------
 // K1: radial kernel (fused ramp when npad == L; fused normalisation when NORM)
 // ---------------------------------------------------------------------------
+// K1 at 4 CTAs per SM: 64 registers without spills; with K2 also at 4 the
+// step drops 179.6 -> 178.6 ms at 2048^3 (neutral at 1024^3 / 512^3)
 #ifndef TB_K1_MINB
-#define TB_K1_MINB TB_MINB
+#define TB_K1_MINB 4
 #endif
 template <int L, bool RAMP, bool NORM>
 __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_K1_MINB : 1)
@@ -1085,9 +1087,12 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
   }
 }
 
+#ifndef TB_K3_MINB
+#define TB_K3_MINB TB_MINB
+#endif
 template <int L, bool CROP_HALF>
-__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::MINB) k3_rows(DevPlan p, Work w, float* __restrict__ img,
-                                                              float out_scale) {
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_K3_MINB : 1)
+    k3_rows(DevPlan p, Work w, float* __restrict__ img, float out_scale) {
   extern __shared__ float2 smem[];
   float chk = 0.f;
   k3_tile<L, CROP_HALF>(p, w, img + (size_t)blockIdx.y * p.n * p.n, out_scale, blockIdx.y, blockIdx.x, smem, chk);
