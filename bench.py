@@ -332,7 +332,9 @@ def run_ours(args):
             mhz = (clk or {}).get("sm_mhz") or 1965.0
             floor_ms = wi / (sms * 4 * mhz * 1e6) * 1e3
             issue = {"bound": "issue", "warp_inst_per_step": wi, "floor_ms": floor_ms,
-                     "frac": floor_ms / ms_step, "source": tr.get("source")}
+                     "frac": floor_ms / ms_step, "source": tr.get("source"),
+                     # FP32 (FMA pipe) utilisation per kernel: the SURVEY 8d co-bound
+                     "fp32_pipe_pct": {k: v.get("fp32_pipe_pct") for k, v in tr["kernels"].items()}}
     except Exception:
         pass
     nat.read_status(ws)

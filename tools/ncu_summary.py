@@ -116,7 +116,8 @@ def main(src, dst):
         if "dram_read" in m and "dram_write" in m and spl:
             traffic["kernels"][k] = {"dram_bytes_per_launch": m["dram_read"] + m["dram_write"],
                                      "dram_bytes_per_slice": (m["dram_read"] + m["dram_write"]) / spl,
-                                     "warp_inst_per_slice": m.get("warp_inst", 0.0) / spl}
+                                     "warp_inst_per_slice": m.get("warp_inst", 0.0) / spl,
+                                     "fp32_pipe_pct": m.get("fma_pipe_pct")}
     with open(os.path.join(os.path.dirname(dst.rstrip("/")), "ncu_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     with open(os.path.join(dst, "ncu_summary.json"), "w") as f:
