@@ -82,7 +82,7 @@ Layout layout_for(const tb_plan* p, int B) {
   l.rowcoef = take((size_t)B * p->rows * sizeof(float));
   l.part = take((size_t)B * p->groups * std::max(p->S, 1) * sizeof(float));
   l.common = take((size_t)B * p->H * sizeof(float2));
-  l.common2 = take((size_t)B * p->H * sizeof(float2));
+  l.common2 = take((size_t)B * p->dp.c2pitch * sizeof(float2));
   l.coefmean = take((size_t)B * sizeof(float));
   l.columns = take((size_t)B * p->dp.col_slice * sizeof(float2));
   l.filtered = take((size_t)B * p->rows * p->n_t * sizeof(float));
@@ -134,7 +134,10 @@ cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
   res.res.pitch2D.height = (size_t)rows;
   res.res.pitch2D.pitchInBytes = (size_t)p->H * sizeof(float2);
   cudaTextureDesc td{};
-  td.addressMode[0] = cudaAddressModeClamp;
+  // radial texels beyond H - 1 read as 0: nodes outside the disc (table x = H + 1)
+  // gather zeros, and the clamp r1c = min(r0 + 1, H - 1) only matters at
+  // r0 = H - 1, where the radial fraction is exactly 0
+  td.addressMode[0] = cudaAddressModeBorder;
   td.addressMode[1] = cudaAddressModeClamp;
   td.filterMode = cudaFilterModePoint;
   td.readMode = cudaReadModeElementType;
@@ -511,6 +514,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   auto cleanup = [&](int code, const std::string& msg) {
     if (p->blob) cudaFree(p->blob);
     if (p->table) cudaFree(p->table);
+    if (p->table2) cudaFree(p->table2);
     delete p;
     if (prev >= 0) cudaSetDevice(prev);
     return fail(code, msg);
@@ -556,6 +560,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   // per-slice K2 output padded to 128 B: slices never share a cache line
   dp.col_slice = (((size_t)((n + 3) / 4) * (H + 1) * 4 + 15) / 16) * 16;
   dp.prow = d->full_turn ? 2 * V : V + 1;
+  dp.c2pitch = H + 16;  // 128-B aligned rows; entries >= H are zero (outside-disc nodes)
   dp.ss_cs = reinterpret_cast<const double2*>(b + o_ss);
 
   // gridding table (fourier_bp.py:222-249), built on the device in fp64
@@ -569,6 +574,17 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("build_grid_table: ") + cudaGetErrorString(e));
     dp.gridtab = static_cast<const uint2*>(p->table);
+  }
+  dp.gridtab2 = nullptr;
+  if (!d->full_turn && d->interp == TB_INTERP_BILINEAR) {
+    const long long cnt = (long long)(H + 1) * L;
+    e = cudaMalloc(&p->table2, cnt * sizeof(float4));
+    if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc(table2): ") + cudaGetErrorString(e));
+    tb::build_grid_table2<<<(unsigned)((cnt + 255) / 256), 256>>>(static_cast<float4*>(p->table2), H, V, dnu, df,
+                                                                   (2.0 * V) / (2.0 * kPi));
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("build_grid_table2: ") + cudaGetErrorString(e));
+    dp.gridtab2 = static_cast<const float4*>(p->table2);
   }
 
   int rc = configure_dispatch(p);
@@ -590,6 +606,7 @@ int tb_plan_destroy(tb_plan* p) {
     for (auto& t : p->texs) cudaDestroyTextureObject(t.obj);
     cudaFree(p->blob);
     if (p->table) cudaFree(p->table);
+    if (p->table2) cudaFree(p->table2);
     if (prev >= 0) cudaSetDevice(prev);
   }
   delete p;

@@ -46,6 +46,12 @@ struct DevPlan {
   const float2* modt;   // [L]    half-node modulation (or null)
   const double2* ss_cs; // [A]    (cos, sin) of the input angles
   const uint2* gridtab; // [(H+1)^2] first-quadrant gridding table
+  // [(H+1)][L] half-plane gridding table of the half-turn bilinear path:
+  // per Cartesian node (column a, row b) the texel coordinates and fp32
+  // weights of the polar sample actually read (lower half plane already
+  // reflected), or null
+  const float4* gridtab2;
+  int c2pitch;          // elements per slice of Work::common2 (>= H + 1; [H..] = 0)
   int prow;             // polar rows per slice: V + 1 (half turn, row V = conj row 0) or 2V
   size_t col_slice;     // complex elements per slice of the K2 output (tiled)
 };
@@ -55,7 +61,7 @@ struct Work {
   float* rowcoef;
   float* part;
   float2* common;
-  float2* common2;  // [B][H] (Re C[r], Re C[min(r+1, H-1)]) for the half-turn fast path
+  float2* common2;  // [B][c2pitch] (Re C[r], Re C[min(r+1, H-1)]) for the half-turn fast path, 0 for r >= H
   float* coefmean;
   float2* columns;
   float* filtered;
@@ -490,8 +496,9 @@ __device__ __forceinline__ void k1b_slice(const DevPlan& p, const Work& w, int q
   }
   if (t == 0) w.coefmean[q] = amean + c;
   __syncthreads();
-  float2* out2 = w.common2 + (size_t)q * H;
-  for (int k = t; k < H; k += blockDim.x) out2[k] = make_float2(buf2[k], buf2[min(k + 1, H - 1)]);
+  float2* out2 = w.common2 + (size_t)q * p.c2pitch;
+  for (int k = t; k < p.c2pitch; k += blockDim.x)
+    out2[k] = k < H ? make_float2(buf2[k], buf2[min(k + 1, H - 1)]) : make_float2(0.f, 0.f);
 }
 
 template <int L>
@@ -535,6 +542,51 @@ __global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab,
   uint2 e;
   e.x = (uint32_t)(inside ? (r0 & 0xFFFF) : 0xFFFF) | ((uint32_t)t0 << 16);
   e.y = (uint32_t)qr | ((uint32_t)qt << 16);
+  tab[i] = e;
+}
+
+// Half-plane table of the half-turn bilinear path (fourier_bp.py:222-249 per
+// node, fp64): entry [a][b] for column a in [0, H] (a = H is -L/2) and row
+// b in [0, L).  Rows b >= H (signed b < 0) are evaluated as the conjugate of
+// the point reflection (-a, -b) (upper half plane, polar rows t in [0, V],
+// row V = conj row 0), so every entry addresses rows <= V:
+//   x = ra + 1   texel coordinate of the 2x2 TLD4 footprint (ra, ra + 1);
+//                H + 1 outside the disc (border texels: the gather is 0, and
+//                common2[H] = 0)
+//   y = t0 + 1   row coordinate within the slice's V + 1 rows
+//   z, w = rf, tf  bilinear fractions, fp64-computed, rounded to fp32
+__global__ void __launch_bounds__(256) build_grid_table2(float4* __restrict__ tab, int H, int V, double dnu,
+                                                         double df, double tscale) {
+  const int L = 2 * H;
+  const long long count = (long long)(H + 1) * L;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int a = (int)(i / L), b = (int)(i % L);
+  int ea = a < H ? a : -H, eb = b < H ? b : b - L;
+  if (eb < 0) {  // reflected: conj C(-a, -b); -(-H) is the same node (magnitude H)
+    ea = -ea;
+    eb = -eb;
+  }
+  const double nu1 = ((double)ea * (1.0 / L)) * L * dnu;
+  const double nu2 = ((double)eb * (1.0 / L)) * L * dnu;
+  const double ri = hypot(nu1, nu2) / df;
+  double ph = atan2(nu2, nu1);
+  if (ph < 0.0) ph += 2.0 * 3.14159265358979323846;  // np.mod(., 2 pi); nu2 >= 0 here
+  const double ti = ph * tscale;
+  float4 e;
+  if (ri <= (double)(H - 1)) {
+    const double rfl = floor(ri);
+    double tfl = floor(ti);
+    double tf = ti - tfl;
+    int t0 = (int)tfl;
+    if (t0 >= V) {  // angle pi (t0 = V, tf = 0): read it as row V with weight 1 from row V - 1
+      tf += (double)(t0 - (V - 1));
+      t0 = V - 1;
+    }
+    e = make_float4((float)(rfl + 1.0), (float)(t0 + 1), (float)(ri - rfl), (float)tf);
+  } else {
+    e = make_float4((float)(H + 1), 1.f, 0.f, 0.f);
+  }
   tab[i] = e;
 }
 #endif
@@ -651,10 +703,24 @@ __device__ __forceinline__ uint2 ld_table(const uint2* p) {
   return v;
 }
 
+// half-plane table entry (16 B), streamed past L1
+__device__ __forceinline__ float4 ld_table4(const float4* p) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+
 // K2 kernel: CTA of G column groups (G*TPF = 512 threads for L <= 8192)
 // sweeping a contiguous run of columns G at a time.  Adjacent columns read
 // nearly the same polar lines, so the SM's L1 keeps the shared footprint of
 // the G concurrent columns and of the next step resident.
+#ifndef TB_K2_DIRECT
+// K2_TEX: gathered nodes straight into the FFT registers (1) or staged in
+// the FFT buffer first (0)
+#define TB_K2_DIRECT 0
+#endif
 #ifndef TB_K2_RPT
 #define TB_K2_RPT 16
 #endif
@@ -692,7 +758,14 @@ struct K2Shape {
 // of thread t at smem[i * TPF + t]) so they leave registers during the
 // latency-bound gather; a barrier separates the reload from the first FFT
 // pass, which rewrites the buffer.
-template <int L, bool CROP_HALF, class Sync>
+// K2 gather variants, chosen per plan on the host (each its own kernel so
+// ptxas allocates registers for one path only):
+//   K2_TEX   half-turn bilinear, TLD4 gathers driven by the half-plane table
+//   K2_PLAIN half-turn bilinear, plain loads (polar texture view unavailable)
+//   K2_ANY   full-turn input or nearest interpolation (lattice_value)
+enum { K2_ANY = 0, K2_PLAIN = 1, K2_TEX = 2 };
+
+template <int L, bool CROP_HALF, int PATH, class Sync>
 __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a, int q, int t, bool active,
                                           float2* smem, Sync sync) {
   float2* stg = smem;
@@ -704,13 +777,13 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
   const float2* com = w.common + (size_t)q * H;
   const uint2* tab = p.gridtab;
   float2 v[RPT];
-  if (p.interp == 0 && !p.full_turn) {
+  if constexpr (PATH != K2_ANY) {
     // Half-turn bilinear fast path.  A node in the lower half plane (b < 0)
     // is the conjugate of its point reflection (-a, -b), which lies in the
     // upper half plane and reads polar rows t in [0, V] (row V = conj row 0):
     // no per-corner mirror logic.  Groups of NB nodes: the table entries of
     // the next group load while this group's corners are gathered.
-    const float2* com2 = w.common2 + (size_t)q * H;
+    const float2* com2 = w.common2 + (size_t)q * p.c2pitch;
     const uint2* trow = tab + (size_t)a * (H + 1);
     const int V = p.n_theta;
     // M[a] M[b] with M[b] = M[t] M[TPF i]: the column factor M[a] folds into
@@ -721,70 +794,55 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
 #define TB_K2_NB 4
 #endif
     constexpr int NB = TB_K2_NB < RPT ? TB_K2_NB : RPT;
-    if (w.polar_tex) {
-    // three-stage software pipeline over groups of NP nodes: table entries
-    // AH + 1 groups ahead, texture gathers AH groups ahead, bilinear of this
-    // group (the gathers of the next groups are in flight while this one
-    // computes; measured K2 -5 % against issue-then-consume groups)
-    // measured: L = 4096 two nodes per stage one stage ahead (K2 101.8 ->
-    // 101.4 ms at 2048^3); smaller L one node per stage two ahead (the
-    // two-node form is 1-3 % slower there)
+    if constexpr (PATH == K2_TEX) {
+    // three-stage software pipeline over groups of NP nodes: half-plane
+    // table entries (16 B, coalesced) AH + 1 groups ahead, two TLD4 gathers
+    // plus the common-row pair AH groups ahead, bilinear of this group.
+    // Every entry already names the polar texels of the node actually read
+    // (reflection resolved at plan time), so a node costs one table load, a
+    // slice offset, two gathers, one common-row load and the interpolation;
+    // nodes outside the disc read border texels (0) and common2[H] (0)
+    // measured at 2048^3 (K2 ms, slice-fast grid): (NP, AH) = (1, 2) 87.1,
+    // (2, 1) 91.3, (2, 2) 89.8, (4, 1) 90.4; gathering straight into the FFT
+    // registers instead of staging: (1, 2) 99.4, (2, 1) 101.2 (64 registers)
 #ifdef TB_K2_NP
     constexpr int NP0 = TB_K2_NP;
 #else
-    constexpr int NP0 = L == 4096 ? 2 : 1;
+    constexpr int NP0 = 1;
 #endif
 #ifdef TB_K2_AHEAD
     constexpr int AH = TB_K2_AHEAD;
 #else
-    constexpr int AH = L == 4096 ? 1 : 2;
+    constexpr int AH = 2;
 #endif
     constexpr int NP = NP0 < RPT ? NP0 : RPT, NG = RPT / NP;
-    uint2 e[RPT];
+    const float4* trow2 = p.gridtab2 + (size_t)a * L + t;
+    const float fyoff = (float)(q * (V + 1));
+    float4 e[RPT];
     float4 fre[RPT], fim[RPT];
-    // t < TPF: node b = t + i TPF lies in the lower half plane (b >= H,
-    // signed b < 0) exactly when i >= RPT/2 -- a compile-time split; there
-    // the table row is read at L - b (= H for b = H, the same entry)
-    auto tload = [&](int i) {
-      const int b = t + i * TPF;
-      const int ab = i < RPT / 2 ? b : L - b;
-      e[i] = active ? ld_table(trow + ab) : make_uint2(0xFFFFu, 0u);
-    };
+    float2 cc[RPT];
+    auto tload = [&](int i) { e[i] = ld_table4(trow2 + i * TPF); };
     auto fetch = [&](int i) {
-      const uint2 ej = e[i];
-      const int r0 = (int)(ej.x & 0xFFFFu);
-      const int ra = r0 == 0xFFFF ? 0 : r0;
-      const int I = (int)(ej.x >> 16);
-      const int qt = (int)(ej.y >> 16);
-      const bool flip = (as < 0) != (i >= RPT / 2);
-      const int t0 = flip ? (qt ? V - I - 1 : V - I) : I;
-      fre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      fim[i] = fre[i];
-      if (r0 != 0xFFFF) {
-        const float fx = (float)(ra + 1), fy = (float)(q * (p.n_theta + 1) + t0 + 1);
-        fre[i] = tex2Dgather<float4>(w.polar_tex, fx, fy, 0);
-        fim[i] = tex2Dgather<float4>(w.polar_tex, fx, fy, 1);
-      }
+      fre[i] = tex2Dgather<float4>(w.polar_tex, e[i].x, e[i].y + fyoff, 0);
+      fim[i] = tex2Dgather<float4>(w.polar_tex, e[i].x, e[i].y + fyoff, 1);
+      cc[i] = __ldg(com2 + ((int)e[i].x - 1));
     };
     auto consume = [&](int i) {
-      const uint2 ej = e[i];
-      const int r0 = (int)(ej.x & 0xFFFFu);
-      const int ra = r0 == 0xFFFF ? 0 : r0;
-      int qt = (int)(ej.y >> 16);
-      const bool flip = (as < 0) != (i >= RPT / 2);
-      if (flip) qt = qt ? 65536 - qt : 0;
-      const float r = (float)(ej.y & 0xFFFFu) * (1.f / 65536.f), u = (float)qt * (1.f / 65536.f);
+      const float r = e[i].z, u = e[i].w;
       const float4 re = fre[i], im = fim[i];
       const float2 p00 = make_float2(re.w, im.w), p01 = make_float2(re.z, im.z);
       const float2 p10 = make_float2(re.x, im.x), p11 = make_float2(re.y, im.y);
-      const float2 cc = __ldg(com2 + ra);
       const float2 r0v = make_float2(fmaf(r, p01.x - p00.x, p00.x), fmaf(r, p01.y - p00.y, p00.y));
       const float2 r1v = make_float2(fmaf(r, p11.x - p10.x, p10.x), fmaf(r, p11.y - p10.y, p10.y));
-      float2 val = make_float2(fmaf(u, r1v.x - r0v.x, r0v.x) + fmaf(r, cc.y - cc.x, cc.x),
+      float2 val = make_float2(fmaf(u, r1v.x - r0v.x, r0v.x) + fmaf(r, cc[i].y - cc[i].x, cc[i].x),
                                fmaf(u, r1v.y - r0v.y, r0v.y));
-      if (i >= RPT / 2) val.y = -val.y;
+      if (i >= RPT / 2) val.y = -val.y;  // lower half plane: conjugate of the reflection
       if (p.has_mod) val = cmul(val, cmul(m_t, __ldg(p.modt + i * TPF)));
-      if (active) stg[i * TPF + t] = r0 == 0xFFFF ? make_float2(0.f, 0.f) : val;
+#if TB_K2_DIRECT
+      v[i] = active ? val : make_float2(0.f, 0.f);
+#else
+      if (active) stg[i * TPF + t] = val;
+#endif
     };
 #pragma unroll
     for (int i = 0; i < (AH + 1) * NP && i < RPT; ++i) tload(i);
@@ -844,29 +902,11 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
         }
         const float2 z = make_float2(0.f, 0.f);
         const bool in = r0 != 0xFFFF;  // nodes outside the disc are masked below
-        if (w.polar_tex) {
-          // one 2x2 texel gather per component (TLD4, point sampling: exact
-          // fp32 texels; the bilinear weights stay in fp32 below).  Texel
-          // (u, v) = (r, t); clamp addressing reproduces min(r0 + 1, H - 1).
-          const float fx = (float)(ra + 1), fy = (float)(q * (p.n_theta + 1) + t0 + 1);
-          // nodes outside the disc (contiguous runs of b per column: whole
-          // warps) skip their gathers
-          float4 re = make_float4(0.f, 0.f, 0.f, 0.f), im = re;
-          if (in) {
-            re = tex2Dgather<float4>(w.polar_tex, fx, fy, 0);
-            im = tex2Dgather<float4>(w.polar_tex, fx, fy, 1);
-          }
-          p00[j] = make_float2(re.w, im.w);  // (u0, v0) = (ra, t0)
-          p01[j] = make_float2(re.z, im.z);  // (u1, v0) = (rb, t0)
-          p10[j] = make_float2(re.x, im.x);  // (u0, v1) = (ra, t0 + 1)
-          p11[j] = make_float2(re.y, im.y);  // (u1, v1) = (rb, t0 + 1)
-        } else {
-          const float2* row0 = pol + (size_t)t0 * H;
-          p00[j] = in ? __ldg(row0 + ra) : z;
-          p01[j] = in ? __ldg(row0 + rb) : z;
-          p10[j] = in ? __ldg(row0 + H + ra) : z;
-          p11[j] = in ? __ldg(row0 + H + rb) : z;
-        }
+        const float2* row0 = pol + (size_t)t0 * H;
+        p00[j] = in ? __ldg(row0 + ra) : z;
+        p01[j] = in ? __ldg(row0 + rb) : z;
+        p10[j] = in ? __ldg(row0 + H + ra) : z;
+        p11[j] = in ? __ldg(row0 + H + rb) : z;
         cc[j] = __ldg(com2 + ra);
         // M[b] = M[t] * M[TPF*i] (linear phase in the signed index): one
         // per-thread load plus a warp-uniform one instead of a load per node
@@ -889,6 +929,13 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       }
     }
     }
+#if TB_K2_DIRECT
+    if (PATH == K2_TEX && p.nyq && active) {
+      // the Nyquist fix-up below works on the (thread-private) staging slots
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) stg[i * TPF + t] = v[i];
+    }
+#endif
     if (p.nyq && active) {
       // Nyquist lines: Hermitian part 0.5 (C[k] + conj C[-k mod L]) of the fully
       // modulated lattice (.real of ifft2, fourier_bp.py:431)
@@ -905,9 +952,11 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
         }
       }
     }
+    if (PATH != K2_TEX || !TB_K2_DIRECT || p.nyq) {
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) v[i] = active ? stg[i * TPF + t] : make_float2(0.f, 0.f);
-    sync();  // every thread holds its nodes before the FFT rewrites the buffer
+      for (int i = 0; i < RPT; ++i) v[i] = active ? stg[i * TPF + t] : make_float2(0.f, 0.f);
+      sync();  // every thread holds its nodes before the FFT rewrites the buffer
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -941,8 +990,9 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
   }
 }
 
-template <int L, bool CROP_HALF>
-__global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_columns(DevPlan p, Work w, int cols_per_cta) {
+template <int L, bool CROP_HALF, int PATH>
+__global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB)
+    k2_columns(DevPlan p, Work w, int cols_per_cta, int slices_per_cta, int n_slices, int slice_fast) {
   using K2 = K2Shape<L>;
   constexpr int TPF = K2::TPF;
   constexpr int H = L / 2;
@@ -950,30 +1000,39 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB) k2_colu
   const int g = threadIdx.x / TPF;
   const int t = threadIdx.x % TPF;
   float2* buf = smem + g * K2::SMEM_PER_GROUP;
-  const int q = blockIdx.y;
-  const int c0 = blockIdx.x * cols_per_cta;
+  // CTA = a run of columns x a run of slices; slice_fast puts the slice runs
+  // on blockIdx.x so the resident CTAs share their columns' table rows
+  const int cg = slice_fast ? blockIdx.y : blockIdx.x;
+  const int sg = slice_fast ? blockIdx.x : blockIdx.y;
+  const int q0 = sg * slices_per_cta;
+  const int q1 = min(n_slices, q0 + slices_per_cta);
+  const int c0 = cg * cols_per_cta;
   const int c1 = min(H + 1, c0 + cols_per_cta);
   if constexpr (K2::G == 1) {
-    for (int a = c0; a < c1; ++a) {
-      k2_column<L, CROP_HALF>(p, w, a, q, t, true, buf, CtaSync());
-      __syncthreads();  // buffer reuse by the next column
-    }
+    for (int a = c0; a < c1; ++a)
+      for (int q = q0; q < q1; ++q) {
+        k2_column<L, CROP_HALF, PATH>(p, w, a, q, t, true, buf, CtaSync());
+        __syncthreads();  // buffer reuse by the next column
+      }
   } else if constexpr (TPF % 32 == 0 && K2::G < 16 && TB_K2_NAMED) {
     // G column groups side by side on one SM (adjacent columns at the same
     // time share their polar lines in L1), each synchronising only itself
     // through its own named barrier: no coupling between the groups
     const GroupSync gs{1 + g, TPF};
-    for (int a = c0 + g; a < c1; a += K2::G) {
-      k2_column<L, CROP_HALF>(p, w, a, q, t, true, buf, gs);
-      gs();  // buffer reuse by the next column
-    }
+    for (int a = c0 + g; a < c1; a += K2::G)
+      for (int q = q0; q < q1; ++q) {
+        k2_column<L, CROP_HALF, PATH>(p, w, a, q, t, true, buf, gs);
+        gs();  // buffer reuse by the next column
+      }
   } else {
     // sub-warp groups (small L): CTA-wide barriers, idle groups on the tail
     for (int base = c0; base < c1; base += K2::G) {
       const int a = base + g;
       const bool valid = a < c1;
-      k2_column<L, CROP_HALF>(p, w, valid ? a : c1 - 1, q, t, valid, buf, CtaSync());
-      __syncthreads();  // buffer reuse by the next column
+      for (int q = q0; q < q1; ++q) {
+        k2_column<L, CROP_HALF, PATH>(p, w, valid ? a : c1 - 1, q, t, valid, buf, CtaSync());
+        __syncthreads();  // buffer reuse by the next column
+      }
     }
   }
 }

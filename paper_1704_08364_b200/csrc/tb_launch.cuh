@@ -43,6 +43,7 @@ struct tb_plan {
   DevPlan dp;
   void* blob = nullptr;   // all small device tables in one allocation
   void* table = nullptr;  // gridding table [(H+1)^2] uint2
+  void* table2 = nullptr; // half-plane gridding table [(H+1)][L] float4 (half-turn bilinear)
   // texture objects over workspace polar regions, keyed by (pointer, rows);
   // kept until the plan is destroyed (kernels may still be using them)
   struct Tex {
@@ -73,9 +74,13 @@ struct Launch {
   using K2 = tb::K2Shape<L>;
   static size_t smem_k2() { return (size_t)K2::G * K2::SMEM_PER_GROUP * sizeof(float2); }
   // columns per K2 CTA: one resident CTA per SM sweeping G columns at a time
-  static int k2_cols(const tb_plan* p) {
+  static int k2_cols(const tb_plan* p, bool tex) {
     if (const char* e = std::getenv("TB_K2_COLS"))  // tuning: columns swept per CTA
       if (std::atoi(e) > 0) return K2::G * std::atoi(e);
+    // half-plane-table path: slice-fast grid, one column group per CTA (the
+    // resident CTAs cover a few columns of every slice of the launch group,
+    // so each 16 B-per-node table row is read from DRAM once per group)
+    if (tex) return K2::G;
     const int resident = K2::MINB;  // CTAs per SM
     int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
     // L = 4096: the resident CTAs should cover a little less than one slice,
@@ -85,15 +90,45 @@ struct Launch {
     return K2::G * std::max(1, steps);
   }
 
+  // slices per K2 CTA (TB_K2_SPC, tuning; default 1) and the grid order
+  // (TB_K2_ORDER=1: slice runs on blockIdx.x, resident CTAs share columns)
+  static int k2_slices(int B) {
+    if (const char* e = std::getenv("TB_K2_SPC"))
+      if (std::atoi(e) > 0) return std::min(B, std::atoi(e));
+    return 1;
+  }
+  static int k2_slice_fast(bool tex) {
+    if (const char* e = std::getenv("TB_K2_ORDER")) return std::atoi(e) == 1 ? 1 : 0;
+    return tex ? 1 : 0;
+  }
+
+  template <bool CH>
+  static cudaError_t set_k2_smem() {
+    const auto a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_ANY>, a, (int)smem_k2());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_PLAIN>, a, (int)smem_k2());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_TEX>, a, (int)smem_k2());
+    return e;
+  }
+  template <bool CH>
+  static void launch_k2(const DevPlan& dp, const Work& w, dim3 g2, cudaStream_t st, int kc, int spc, int B, int sf) {
+    if (dp.full_turn || dp.interp != 0)
+      tb::k2_columns<L, CH, tb::K2_ANY><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
+    else if (w.polar_tex && dp.gridtab2)
+      tb::k2_columns<L, CH, tb::K2_TEX><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
+    else
+      tb::k2_columns<L, CH, tb::K2_PLAIN><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
+  }
+
   static int configure(tb_plan* p) {
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
     TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
+    TB_CUDA(set_k2_smem<false>());
     TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     if constexpr (L >= 64) {
-      TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k2()));
+      TB_CUDA(set_k2_smem<true>());
       TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     }
     TB_CUDA(cudaFuncSetAttribute(tb::kr_ramp<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
@@ -106,7 +141,7 @@ struct Launch {
         const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
         TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, co, c1));
         TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, co, c1));
-        TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, (L >= 64)>, co, c2));
+        TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, (L >= 64), tb::K2_TEX>, co, c2));
         TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, (L >= 64)>, co, c3));
       }
     }
@@ -154,12 +189,16 @@ struct Launch {
     mark(2, 1);
     const bool half = L >= 64 && 2 * p->n == L;
     mark(3, 0);
-    const int kc = k2_cols(p);
-    const dim3 g2((p->H + 1 + kc - 1) / kc, B);
+    const bool tex = !dp.full_turn && dp.interp == 0 && w.polar_tex && dp.gridtab2;
+    const int kc = k2_cols(p, tex);
+    const int spc = k2_slices(B);
+    const int ncg = (p->H + 1 + kc - 1) / kc, nsg = (B + spc - 1) / spc;
+    const int sf = k2_slice_fast(tex);
+    const dim3 g2(sf ? nsg : ncg, sf ? ncg : nsg);
     if (half)
-      tb::k2_columns<L, (L >= 64)><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
+      launch_k2<(L >= 64)>(dp, w, g2, st, kc, spc, B, sf);
     else
-      tb::k2_columns<L, false><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc);
+      launch_k2<false>(dp, w, g2, st, kc, spc, B, sf);
     mark(3, 1);
     mark(4, 0);
     if (half)

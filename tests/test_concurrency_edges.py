@@ -72,8 +72,10 @@ def test_single_slice_api_equals_volume_slice():
 
 def test_plain_gather_path_matches_texture_path():
     """A launch group whose polar rows exceed the pitch-2D texture height
-    (batch * (n_theta + 1) > 65000) gathers with plain loads instead of TLD4;
-    both paths compute the same bilinear weights on the same fp32 texels."""
+    (batch * (n_theta + 1) > 65000) gathers with plain loads instead of TLD4.
+    Both read the same fp32 texels; the TLD4 path's weights come from the
+    fp32 half-plane table, the plain path's from the unorm16 first-quadrant
+    table (<= 2^-17 weight error), so they agree to ~1e-6, not bitwise."""
     F = _F()
     from paper_1704_08364_b200 import phantom
     plan = F.BstPlan(64, 2048)
@@ -82,4 +84,4 @@ def test_plain_gather_path_matches_texture_path():
     tex = F.fbp_volume(vol, plan, batch=1)     # 2049 rows: texture gathers
     plain = F.fbp_volume(vol, plan, batch=40)  # 81960 rows: plain loads
     rel = (torch.linalg.norm(tex - plain) / torch.linalg.norm(tex)).item()
-    assert rel < 1e-6, rel
+    assert rel < 5e-6, rel
