@@ -8,6 +8,7 @@
  *   tb_plan_create / tb_plan_destroy  <- BstPlan + FilterPlan      fourier_bp.py:69-267
  *   tb_fbp        (kernel "bst")      <- fbp                       fourier_bp.py:508-530
  *   tb_bst                            <- bst_backproject           fourier_bp.py:435-461
+ *   tb_bst_scaled                     <- backproject stage         pipeline.py:511-518
  *   tb_ramp                           <- ramp_filter               fourier_bp.py:490-505
  *   tb_ss         (kernel "ss")       <- backproject_ss            projector.py:126-158
  *   tb_fbp_ss                         <- fbp(kernel="ss")          fourier_bp.py:525-527
@@ -43,7 +44,7 @@
 extern "C" {
 #endif
 
-#define TB_ABI_VERSION 1
+#define TB_ABI_VERSION 2
 
 typedef enum {
   TB_OK = 0,
@@ -73,7 +74,20 @@ typedef struct {
   int32_t full_turn;      /* input holds 2*n_theta angles on [0, 2 pi)     */
   int32_t filter_kind;    /* tb_filter_kind                                */
   double rolloff;         /* (0, 1]; used when filter_kind is apodized     */
+  int32_t n_angles;       /* rows of the input sinogram; 0 -> n_theta (half
+                             turn) or 2 n_theta (full turn).  Any other
+                             count (an odd full turn) only serves the ramp,
+                             slant-stack and forward paths, like the
+                             reference's backproject_ss (projector.py:126-158);
+                             its BST calls fail with TB_ERR_INVALID as the
+                             reference's resample_polar does (fourier_bp.py:331-332) */
+  int32_t flags;          /* TB_PLAN_* bits                                 */
 } tb_plan_desc;
+
+/* tb_plan_desc.flags: build no gridding tables (a plan that only serves
+ * tb_ramp / tb_ss / tb_fbp_ss / tb_forward / preprocessing; its BST calls
+ * fail with TB_ERR_INVALID). */
+#define TB_PLAN_NO_GRID 1
 
 typedef struct {
   int32_t n_t, n_theta, n_angles; /* n_angles = rows in the input sinogram  */
@@ -169,6 +183,12 @@ int tb_rings(const tb_plan* plan, const float* sino, float* out, int window, dou
 /* BST backprojection only (input already ramp-filtered; no 1/(2 pi)). */
 int tb_bst(const tb_plan* plan, const float* sino, float* image, int n_slices,
            int batch, void* workspace, size_t workspace_bytes, void* stream);
+
+/* tb_bst with the output multiplied by `scale` in the last kernel's epilogue
+ * (the reference pipeline's backproject stage, bst_backproject x FBP_SCALE,
+ * pipeline.py:511-518, without a separate pass over the images). */
+int tb_bst_scaled(const tb_plan* plan, const float* sino, float* image, int n_slices,
+                  int batch, void* workspace, size_t workspace_bytes, float scale, void* stream);
 
 /* Ramp filter only: out has the input's shape [B][A][n_t]. */
 int tb_ramp(const tb_plan* plan, const float* sino, float* out, int n_slices,

@@ -40,7 +40,12 @@ class tb_plan_desc(ctypes.Structure):
         ("full_turn", ctypes.c_int32),
         ("filter_kind", ctypes.c_int32),
         ("rolloff", ctypes.c_double),
+        ("n_angles", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
+
+
+TB_PLAN_NO_GRID = 1
 
 
 class tb_plan_info(ctypes.Structure):
@@ -84,6 +89,7 @@ def _bind(lib):
         "tb_workspace_get_layout": (I, [P, I, ctypes.POINTER(tb_workspace_layout)]),
         "tb_fbp": (I, [P, P, P, I, I, P, S, P]),
         "tb_bst": (I, [P, P, P, I, I, P, S, P]),
+        "tb_bst_scaled": (I, [P, P, P, I, I, P, S, ctypes.c_float, P]),
         "tb_fbp_profiled": (I, [P, P, P, I, I, P, S, P, ctypes.POINTER(ctypes.c_double)]),
         "tb_ramp": (I, [P, P, P, I, P]),
         "tb_ss": (I, [P, P, P, I, ctypes.c_float, P]),

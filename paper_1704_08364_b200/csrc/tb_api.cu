@@ -219,6 +219,10 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
                  const NormFrames* norm = nullptr, bool frame_major = false) {
   int rc = check_exec_args(p, sino, img, n_slices, batch, ws, ws_bytes);
   if (rc) return rc;
+  if (!p->bst_ok)
+    return fail(TB_ERR_INVALID, p->rows != (p->desc.full_turn ? 2 * p->V : p->V)
+                                    ? "sinogram dimensions do not match the plan"
+                                    : "plan was created without gridding tables (TB_PLAN_NO_GRID)");
   if ((rc = set_device(p))) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float2* normtab = nullptr;
@@ -340,13 +344,18 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
     return fail(TB_ERR_INVALID, "rolloff must be in (0, 1]");
   if (!(d->kb_support > 0.0)) return fail(TB_ERR_INVALID, "kb_support must be > 0");
   if (L > kMaxL) return fail(TB_ERR_UNSUPPORTED, "radial_samples > 8192 is not supported on the GPU path");
+  const int rows_std = d->full_turn ? 2 * d->n_theta : d->n_theta;
+  if (d->n_angles < 0) return fail(TB_ERR_INVALID, "n_angles must be >= 0");
+  if (d->flags & ~TB_PLAN_NO_GRID) return fail(TB_ERR_INVALID, "unknown plan flags");
 
   tb_plan* p = new tb_plan();
   p->desc = *d;
   p->device = device;
   p->n_t = d->n_t;
   p->V = d->n_theta;
-  p->rows = d->full_turn ? 2 * d->n_theta : d->n_theta;
+  p->rows = d->n_angles > 0 ? d->n_angles : rows_std;
+  // the BST chain needs the standard layout and the gridding tables
+  p->bst_ok = p->rows == rows_std && !(d->flags & TB_PLAN_NO_GRID);
   p->L = (int)L;
   p->H = (int)L / 2;
   p->n = n;
@@ -564,8 +573,10 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   dp.ss_cs = reinterpret_cast<const double2*>(b + o_ss);
 
   // gridding table (fourier_bp.py:222-249), built on the device in fp64
-  if ((long long)V / 2 >= 65535) return cleanup(TB_ERR_UNSUPPORTED, "n_theta too large for the gridding table");
-  {
+  if (p->bst_ok && (long long)V / 2 >= 65535)
+    return cleanup(TB_ERR_UNSUPPORTED, "n_theta too large for the gridding table");
+  dp.gridtab = nullptr;
+  if (p->bst_ok) {
     const long long cnt = (long long)(H + 1) * (H + 1);
     e = cudaMalloc(&p->table, cnt * sizeof(uint2));
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc(table): ") + cudaGetErrorString(e));
@@ -576,7 +587,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
     dp.gridtab = static_cast<const uint2*>(p->table);
   }
   dp.gridtab2 = nullptr;
-  if (!d->full_turn && d->interp == TB_INTERP_BILINEAR) {
+  if (p->bst_ok && !d->full_turn && d->interp == TB_INTERP_BILINEAR) {
     const long long cnt = (long long)(H + 1) * L;
     e = cudaMalloc(&p->table2, cnt * sizeof(float4));
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc(table2): ") + cudaGetErrorString(e));
@@ -603,6 +614,9 @@ int tb_plan_destroy(tb_plan* p) {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
+    // calls are asynchronous: kernels enqueued with this plan (on any
+    // stream) may still read its tables and texture objects
+    cudaDeviceSynchronize();
     for (auto& t : p->texs) cudaDestroyTextureObject(t.obj);
     cudaFree(p->blob);
     if (p->table) cudaFree(p->table);
@@ -705,6 +719,11 @@ int tb_normalize(const tb_plan* p, const float* counts, const float* flat, const
 int tb_bst(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws, size_t ws_bytes,
            void* stream) {
   return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, false, 1.0f);
+}
+
+int tb_bst_scaled(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws,
+                  size_t ws_bytes, float scale, void* stream) {
+  return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, false, scale);
 }
 
 int tb_ramp(const tb_plan* p, const float* sino, float* out, int n_slices, void* stream) {

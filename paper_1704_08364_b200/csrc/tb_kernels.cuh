@@ -530,15 +530,24 @@ __global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab,
   const double ri = hypot(nu1, nu2) / df;
   const double tq = atan2(nu2, nu1) * tscale;
   const int top = H - 1;
-  double rfl = floor(ri);
-  int r0 = (int)rfl;
-  int qr = (int)rint((ri - rfl) * 65536.0);
-  if (qr >= 65536) { qr = 0; ++r0; }
-  double tfl = floor(tq);
-  int t0 = (int)tfl;
-  int qt = (int)rint((tq - tfl) * 65536.0);
-  if (qt >= 65536) { qt = 0; ++t0; }
-  const bool inside = nearest ? (rint(ri) <= (double)top) : (ri <= (double)top);
+  int r0, qr, t0, qt;
+  if (nearest) {
+    // np.rint (half to even) decided here in fp64 (fourier_bp.py:234-236):
+    // the entry holds the rounded indices with zero fractions
+    r0 = (int)rint(ri);
+    t0 = (int)rint(tq);
+    qr = qt = 0;
+  } else {
+    const double rfl = floor(ri);
+    r0 = (int)rfl;
+    qr = (int)rint((ri - rfl) * 65536.0);
+    if (qr >= 65536) { qr = 0; ++r0; }
+    const double tfl = floor(tq);
+    t0 = (int)tfl;
+    qt = (int)rint((tq - tfl) * 65536.0);
+    if (qt >= 65536) { qt = 0; ++t0; }
+  }
+  const bool inside = nearest ? (r0 <= top) : (ri <= (double)top);
   uint2 e;
   e.x = (uint32_t)(inside ? (r0 & 0xFFFF) : 0xFFFF) | ((uint32_t)t0 << 16);
   e.y = (uint32_t)qr | ((uint32_t)qt << 16);

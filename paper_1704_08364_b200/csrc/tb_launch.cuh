@@ -40,6 +40,7 @@ struct tb_plan {
   int n_t, V, rows, L, H, n, npad, lo, hi, S;
   double amp;
   int groups, pairs_per_cta;
+  bool bst_ok = true;  // standard angle layout and gridding tables present
   DevPlan dp;
   void* blob = nullptr;   // all small device tables in one allocation
   void* table = nullptr;  // gridding table [(H+1)^2] uint2
@@ -121,10 +122,19 @@ struct Launch {
   }
 
   static int configure(tb_plan* p) {
-    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1(p)));
-    TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k1b(p)));
+    // The dynamic shared-memory limit is a per-kernel (process-wide)
+    // attribute while K1 / K1b need space for the plan's window support S:
+    // size it for the largest S any plan of this L can have (S <= n_t <=
+    // L/2) so a later plan never lowers it below what an earlier one needs
+    // (the limit does not change occupancy; the launch's request does)
+    tb_plan worst;
+    worst.S = L / 2;
+    worst.n_t = L / 2;
+    const int s1 = (int)smem_k1(&worst), s1b = (int)smem_k1b(&worst);
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1b));
     TB_CUDA(set_k2_smem<false>());
     TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
     if constexpr (L >= 64) {

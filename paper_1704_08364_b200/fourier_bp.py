@@ -161,7 +161,8 @@ class NativePlan:
     """Owns one ``tb_plan`` (device constants for a BstPlan x FilterPlan x
     angle span on one device).  Immutable; safe to share across threads."""
 
-    def __init__(self, plan: BstPlan, fplan: FilterPlan, full_turn: bool, device: int):
+    def __init__(self, plan: BstPlan, fplan: FilterPlan, full_turn: bool, device: int,
+                 n_angles: int | None = None, grid: bool = True):
         lib = _native.lib()
         d = _native.tb_plan_desc()
         d.n_t = plan.n_t
@@ -176,6 +177,8 @@ class NativePlan:
         d.full_turn = 1 if full_turn else 0
         d.filter_kind = 1 if fplan.kind == "ramp_apodized" else 0
         d.rolloff = fplan.rolloff
+        d.n_angles = 0 if n_angles is None else int(n_angles)
+        d.flags = 0 if grid else _native.TB_PLAN_NO_GRID
         h = ctypes.c_void_p()
         _native.check(lib.tb_plan_create(ctypes.byref(d), int(device), ctypes.byref(h)), "tb_plan_create")
         self._h = h
@@ -225,12 +228,20 @@ class NativePlan:
         return ctypes.c_void_p(stream.cuda_stream)
 
     def run(self, op: str, sino: torch.Tensor, image: torch.Tensor, n_slices: int, batch: int,
-            workspace: torch.Tensor, stream=None) -> None:
+            workspace: torch.Tensor, stream=None, scale: float | None = None) -> None:
+        """``scale`` (op "bst" only): multiply the backprojection in K3's
+        epilogue (tb_bst_scaled) instead of a separate pass."""
+        args = (self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(image.data_ptr()), int(n_slices),
+                int(batch), ctypes.c_void_p(workspace.data_ptr()), ctypes.c_size_t(workspace.numel()))
+        if scale is not None and op == "bst":
+            rc = self._lib.tb_bst_scaled(*args, ctypes.c_float(scale), self._stream(stream))
+            _native.check(rc, "tb_bst_scaled")
+            return
+        if scale is not None:
+            raise ValueError(f"scale applies to op 'bst' only, not {op!r}")
         fn = {"fbp": self._lib.tb_fbp, "bst": self._lib.tb_bst, "fbp_ss": self._lib.tb_fbp_ss,
               "fbp_frames": self._lib.tb_fbp_frames}[op]
-        rc = fn(self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(image.data_ptr()), int(n_slices),
-                int(batch), ctypes.c_void_p(workspace.data_ptr()), ctypes.c_size_t(workspace.numel()),
-                self._stream(stream))
+        rc = fn(*args, self._stream(stream))
         _native.check(rc, f"tb_{op}")
 
     def run_counts(self, counts: torch.Tensor, flat: torch.Tensor, dark: torch.Tensor, eps: float,
@@ -353,12 +364,40 @@ def _device_index(device=None) -> int:
 
 
 def native_plan(plan: BstPlan, fplan: FilterPlan = FilterPlan(), full_turn: bool = False,
-                device=None) -> NativePlan:
+                device=None, n_angles: int | None = None, grid: bool = True) -> NativePlan:
     """Device plan for (plan, fplan, span) on `device`, cached on the BstPlan
-    like the reference's lazily built tables (fourier_bp.py:154-162)."""
+    like the reference's lazily built tables (fourier_bp.py:154-162).
+    ``grid=False`` skips the gridding tables (ramp / slant-stack / forward
+    / preprocessing use); ``n_angles`` overrides the input row count (an odd
+    full turn for the slant stack)."""
     dev = _device_index(device)
-    key = ("native", fplan.kind, fplan.effective_rolloff, bool(full_turn), dev)
-    return plan._cached(key, lambda: NativePlan(plan, fplan, full_turn, dev))
+    key = ("native", fplan.kind, fplan.effective_rolloff, bool(full_turn), dev, n_angles, bool(grid))
+    return plan._cached(key, lambda: NativePlan(plan, fplan, full_turn, dev, n_angles, grid))
+
+
+_AUX_PLANS: dict = {}
+_AUX_LOCK = threading.Lock()
+
+
+def aux_plan(n_t: int, n_angles: int, full_turn: bool = False, output_n: int | None = None,
+             fplan: FilterPlan = FilterPlan(), device=None) -> NativePlan:
+    """Cached table-free device plan for the ramp, slant-stack, forward and
+    preprocessing calls on a (n_t, n_angles) sinogram grid (and an output_n
+    image grid): no gridding tables, built once per key and device."""
+    dev = _device_index(device)
+    n = n_t if output_n is None else int(output_n)
+    n_theta = n_angles // 2 if full_turn else n_angles
+    L = max(_next_pow2(2 * n_t), _next_pow2(n))
+    key = (n_t, n_angles, bool(full_turn), n, fplan.kind, fplan.effective_rolloff, dev)
+    hit = _AUX_PLANS.get(key)
+    if hit is None:
+        with _AUX_LOCK:
+            hit = _AUX_PLANS.get(key)
+            if hit is None:
+                bp = BstPlan(n_t=max(n_t, 2), n_theta=max(n_theta, 1), radial_samples=L, output_n=n)
+                hit = NativePlan(bp, fplan, full_turn, dev, n_angles=n_angles, grid=False)
+                _AUX_PLANS[key] = hit
+    return hit
 
 
 def _to_device_rows(y: Sinogram, dev: int) -> torch.Tensor:
@@ -370,12 +409,15 @@ def _check_plan(y: Sinogram, plan: BstPlan) -> None:
     if y.n_t != plan.n_t or half != plan.n_theta:
         raise ValueError("sinogram dimensions do not match the plan")
     if y.angles.full_turn and y.n_angles != 2 * plan.n_theta:
-        raise NotImplementedError("full-turn input with an odd angle count is not supported on the GPU path")
+        # the reference's resample_polar rejects it the same way (fourier_bp.py:331-332)
+        raise ValueError("sinogram dimensions do not match the plan")
 
 
-def _single_slice(op: str, y: Sinogram, plan: BstPlan, fplan: FilterPlan, device=None) -> ImageGrid:
+def _single_slice(op: str, y: Sinogram, plan: BstPlan, fplan: FilterPlan, device=None,
+                  nat: NativePlan | None = None) -> ImageGrid:
     dev = _device_index(device)
-    nat = native_plan(plan, fplan, y.angles.full_turn, dev)
+    if nat is None:
+        nat = native_plan(plan, fplan, y.angles.full_turn, dev)
     sino = _to_device_rows(y, dev)
     img = torch.empty((plan.output_n, plan.output_n), dtype=torch.float32, device=f"cuda:{dev}")
     ws = nat.new_workspace(1)
@@ -389,8 +431,7 @@ def _single_slice(op: str, y: Sinogram, plan: BstPlan, fplan: FilterPlan, device
 def ramp_filter(y: Sinogram, fplan: FilterPlan = FilterPlan(), workers: int = 1, device=None) -> Sinogram:
     """Ramp filtering along t on the GPU (fourier_bp.py:490-505)."""
     dev = _device_index(device)
-    rp = BstPlan(n_t=y.n_t, n_theta=y.n_angles)
-    nat = native_plan(rp, fplan, False, dev)
+    nat = aux_plan(y.n_t, y.n_angles, fplan=fplan, device=dev)
     sino = _to_device_rows(y, dev)
     out = torch.empty_like(sino)
     with torch.cuda.device(dev):
@@ -414,9 +455,9 @@ def fbp(y: Sinogram, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     if plan is None:
         plan = BstPlan.for_sinogram(y)
     if kernel == "ss":
-        from .projector import _ss_plan
-        sp = _ss_plan(y, plan.output_n)
-        return _single_slice("fbp_ss", y, sp, fplan, device)
+        dev = _device_index(device)
+        nat = aux_plan(y.n_t, y.n_angles, y.angles.full_turn, plan.output_n, fplan, dev)
+        return _single_slice("fbp_ss", y, plan, fplan, dev, nat)
     _check_plan(y, plan)
     return _single_slice("fbp", y, plan, fplan, device)
 
@@ -472,7 +513,8 @@ def _frames_on(frames, dev: int, A: int, n_t: int):
 def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan(), kernel: str = "bst",
                full_turn: bool = False, out: torch.Tensor | None = None, batch: int | None = None,
                devices=None, chunk: int | None = None, check: bool = True, frames=None,
-               eps: float = 1e-6, center=None, rings: int | None = None) -> torch.Tensor:
+               eps: float = 1e-6, center=None, rings: int | None = None,
+               scale: float | None = None) -> torch.Tensor:
     """Reconstruct a sinogram volume [S][A][n_t] -> image volume [S][n][n].
 
     * CUDA tensor input: computed on that device, asynchronously on the
@@ -498,6 +540,9 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     center and rings stages (pipeline.py:461-484) on the device before the
     reconstruction (device input); an implausible or undetermined centre
     raises CenteringError like the reference.
+
+    ``scale`` (kernel "none" only) multiplies the backprojection inside the
+    last kernel's epilogue (the pipeline's bst_backproject x FBP_SCALE).
     """
     if frames is not None and not eps > 0:
         raise ValueError("eps must be positive")
@@ -515,7 +560,11 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     if n_t != plan.n_t or A != want_a:
         raise ValueError("sinogram dimensions do not match the plan")
     op = {"bst": "fbp", "ss": "fbp_ss", "none": "bst"}[kernel]
+    if scale is not None and kernel != "none":
+        raise ValueError("scale applies to kernel='none' (the fbp kernels carry 1/(2 pi))")
     n = plan.output_n
+    if out is not None:
+        _check_out(out, (S, n, n), sino)
     if batch is None:
         batch = default_batch(plan)
     if (center is not None or rings is not None) and not sino.is_cuda:
@@ -526,7 +575,7 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
         frames = None  # normalised by the preprocessing pass
     if sino.is_cuda:
         dev = sino.device.index
-        nat = native_plan(plan, fplan, full_turn, dev)
+        nat = native_plan(plan, fplan, full_turn, dev, grid=op != "fbp_ss")
         if out is None:
             out = torch.empty((S, n, n), dtype=torch.float32, device=sino.device)
         ws = nat.new_workspace(min(batch, max(S, 1)))
@@ -539,18 +588,36 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
                     flat, dark = _frames_on(frames, dev, A, n_t)
                     line = torch.empty_like(sino)
                     nat.normalize(sino, flat, dark, eps, line, S)
-                    nat.run(op, line, out, S, min(batch, S), ws)
+                    nat.run(op, line, out, S, min(batch, S), ws, scale=scale)
             elif S:
-                nat.run(op, sino, out, S, min(batch, S), ws)
+                nat.run(op, sino, out, S, min(batch, S), ws, scale=scale)
             if check:
                 nat.read_status(ws)
         return out
     if frames is not None and op != "fbp":
         raise ValueError("host-resident counts are supported for kernel 'bst' (fused normalisation)")
-    return _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check, frames, eps)
+    return _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check, frames, eps, scale)
 
 
-def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check, frames=None, eps=1e-6):
+def _check_out(out, shape, sino) -> None:
+    """A caller-supplied output must be exactly what the kernels write: the
+    kernels take a raw pointer (no bounds, dtype or stride information)."""
+    if not isinstance(out, torch.Tensor):
+        raise ValueError("out must be a torch.Tensor")
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if out.dtype != torch.float32:
+        raise ValueError(f"out must be float32, got {out.dtype}")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
+    if sino.is_cuda and out.device != sino.device:
+        raise ValueError(f"out is on {out.device}, the sinogram on {sino.device}")
+    if not sino.is_cuda and out.is_cuda:
+        raise ValueError("out must be a CPU tensor for host-resident input")
+
+
+def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check, frames=None, eps=1e-6,
+                 scale=None):
     S, A, n_t = sino.shape
     n = plan.output_n
     if devices is None:
@@ -571,7 +638,7 @@ def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, c
     for dev, (b, e) in zip(devices, slabs):
         if e <= b:
             continue
-        nat = native_plan(plan, fplan, full_turn, dev)
+        nat = native_plan(plan, fplan, full_turn, dev, grid=op != "fbp_ss")
         m = min(chunk, e - b)
         with torch.cuda.device(dev):
             st = {
@@ -610,7 +677,8 @@ def _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, c
                     st["nat"].counts(st["inb"][k], st["frames"], eps, st["outb"][k], m, min(batch, st["chunk"]),
                                      st["ws"], st["s_cmp"])
                 else:
-                    st["nat"].run(op, st["inb"][k], st["outb"][k], m, min(batch, st["chunk"]), st["ws"], st["s_cmp"])
+                    st["nat"].run(op, st["inb"][k], st["outb"][k], m, min(batch, st["chunk"]), st["ws"], st["s_cmp"],
+                                  scale=scale)
                 st["cmp"][k].record(st["s_cmp"])
                 with torch.cuda.stream(st["s_out"]):
                     st["s_out"].wait_event(st["cmp"][k])

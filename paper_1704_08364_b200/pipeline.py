@@ -18,7 +18,7 @@ from typing import Any, Callable
 import numpy as np
 import torch
 
-from .fourier_bp import BstPlan, FilterPlan, FBP_SCALE, _device_index, fbp_volume, native_plan
+from .fourier_bp import BstPlan, FilterPlan, FBP_SCALE, _device_index, aux_plan, fbp_volume
 from .slices import ImageGrid, Sinogram, StageKind, VolumeBlock
 
 __all__ = ["StageSpec", "block_descriptors", "make_fbp_stage", "make_backproject_stage", "make_filter_stage"]
@@ -84,9 +84,8 @@ def make_backproject_stage(plan: BstPlan, workers: int = 1, queue_capacity: int 
 
     def process(block: VolumeBlock) -> VolumeBlock:
         vol, full = _stack(block, dev)
-        out = fbp_volume(vol, plan, FilterPlan(), kernel="none", full_turn=full)
-        if scale != 1.0:
-            out.mul_(scale)
+        # the scale rides in K3's epilogue (tb_bst_scaled): no extra pass
+        out = fbp_volume(vol, plan, FilterPlan(), kernel="none", full_turn=full, scale=scale)
         return VolumeBlock(block.first_slice, _images(out, plan.output_n), StageKind.BACKPROJECT)
 
     return StageSpec("backproject", workers, queue_capacity, process, 2.0)
@@ -100,8 +99,7 @@ def make_filter_stage(fplan: FilterPlan = FilterPlan(), workers: int = 1, queue_
     def process(block: VolumeBlock) -> VolumeBlock:
         vol, full = _stack(block, dev)
         s0 = block.slices[0]
-        rp = BstPlan(n_t=s0.n_t, n_theta=s0.n_angles)
-        nat = native_plan(rp, fplan, False, dev)
+        nat = aux_plan(s0.n_t, s0.n_angles, fplan=fplan, device=dev)
         out = torch.empty_like(vol)
         with torch.cuda.device(dev):
             nat.ramp(vol, out, vol.shape[0])

@@ -24,9 +24,6 @@ import torch
 __all__ = ["FlatDarkFrames", "normalize", "CenteringError", "CenteringResult", "estimate_center", "apply_center",
            "suppress_rings", "preprocess_volume"]
 
-_PLANS: dict = {}  # (n_angles, n_t) -> BstPlan carrying the device plan for tb_normalize
-
-
 @dataclass(frozen=True)
 class FlatDarkFrames:
     """Flat (no sample) and dark (no beam) detector frames."""
@@ -56,8 +53,7 @@ def normalize(counts: np.ndarray, frames: FlatDarkFrames, eps: float = 1e-6, dev
         raise ValueError("counts must be a [n_angles][n_t] frame")
     a, n_t = counts.shape
     dev = F._device_index(device)
-    plan = _PLANS.setdefault((a, n_t), F.BstPlan(n_t=max(n_t, 2), n_theta=max(a, 1)))
-    nat = F.native_plan(plan, F.FilterPlan(), False, dev)
+    nat = F.aux_plan(n_t, a, device=dev)
     c = torch.from_numpy(counts.astype(np.float32)).to(f"cuda:{dev}")
     flat, dark = F._frames_on(frames, dev, a, n_t)
     out = torch.empty_like(c)
@@ -82,11 +78,6 @@ class CenteringResult:
             raise ValueError("non-finite center estimate")
 
 
-def _rows_plan(n_angles: int, n_t: int):
-    from . import fourier_bp as F
-    return _PLANS.setdefault((n_angles, n_t), F.BstPlan(n_t=max(n_t, 2), n_theta=max(n_angles, 1)))
-
-
 def _on_device(data, dev: int) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32)).to(f"cuda:{dev}")
 
@@ -105,7 +96,7 @@ def estimate_center(y, device=None) -> CenteringResult:
     if y.n_angles < 2:
         raise CenteringError("need at least two projection angles")
     dev = F._device_index(device)
-    nat = F.native_plan(_rows_plan(y.n_angles, y.n_t), F.FilterPlan(), False, dev)
+    nat = F.aux_plan(y.n_t, y.n_angles, device=dev)
     with torch.cuda.device(dev):
         bc, st = nat.center_estimate(_on_device(y.data, dev)[None], 1)
     beta, conf = (float(v) for v in bc[0].cpu())
@@ -121,7 +112,7 @@ def apply_center(y, beta: float, device=None):
     if abs(beta) > y.n_t:
         raise ValueError(f"shift of {beta} bins exceeds the detector extent")
     dev = F._device_index(device)
-    nat = F.native_plan(_rows_plan(y.n_angles, y.n_t), F.FilterPlan(), False, dev)
+    nat = F.aux_plan(y.n_t, y.n_angles, device=dev)
     x = _on_device(y.data, dev)[None]
     out = torch.empty_like(x)
     bc = torch.tensor([[float(beta), 0.0]], dtype=torch.float64, device=f"cuda:{dev}")
@@ -137,7 +128,7 @@ def suppress_rings(y, window: int = 9, device=None):
     if window < 3 or window % 2 == 0:
         raise ValueError(f"window must be an odd integer >= 3, got {window}")
     dev = F._device_index(device)
-    nat = F.native_plan(_rows_plan(y.n_angles, y.n_t), F.FilterPlan(), False, dev)
+    nat = F.aux_plan(y.n_t, y.n_angles, device=dev)
     x = _on_device(y.data, dev)[None]
     out = torch.empty_like(x)
     with torch.cuda.device(dev):
@@ -153,7 +144,7 @@ def preprocess_volume(sino: torch.Tensor, plan, full_turn: bool = False, frames=
     from . import fourier_bp as F
     S, A, n_t = sino.shape
     dev = sino.device.index
-    nat = F.native_plan(plan, F.FilterPlan(), full_turn, dev)
+    nat = F.aux_plan(n_t, A, full_turn, device=dev)
     x = sino
     with torch.cuda.device(dev):
         if frames is not None:

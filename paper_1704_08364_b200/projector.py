@@ -16,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .fourier_bp import BstPlan, FilterPlan, _device_index, native_plan
+from .fourier_bp import FilterPlan, _device_index, aux_plan
 from dataclasses import dataclass
 
 from .slices import AngleAxis, DetectorAxis, ImageGrid, Sinogram
@@ -39,28 +39,17 @@ class RayTraceConfig:
             raise ValueError(f"unknown interpolation {self.interpolation!r}")
 
 
-def _next_pow2(n: int) -> int:
-    m = 1
-    while m < n:
-        m <<= 1
-    return m
-
-
-def _ss_plan(y: Sinogram, n: int) -> BstPlan:
-    """A device plan carrying the slant-stack geometry: the detector axis, the
-    angle span (half or full turn) and the n x n output grid."""
-    if y.angles.full_turn and y.n_angles % 2:
-        raise NotImplementedError("full-turn input with an odd angle count is not supported on the GPU path")
-    n_theta = y.n_angles // 2 if y.angles.full_turn else y.n_angles
-    L = max(_next_pow2(2 * y.n_t), _next_pow2(n))
-    return BstPlan(n_t=y.n_t, n_theta=n_theta, radial_samples=L, output_n=n)
+def _ss_plan(y: Sinogram, n: int, device=None):
+    """Table-free device plan carrying the slant-stack geometry: the
+    detector axis, the angle span and count (any count, odd full turns
+    included, like projector.py:126-158) and the n x n output grid."""
+    return aux_plan(y.n_t, y.n_angles, y.angles.full_turn, n, FilterPlan(), device)
 
 
 def backproject_ss(y: Sinogram, n: int, workers: int = 1, device=None) -> ImageGrid:
     """Slant-stack backprojection onto an n x n grid (projector.py:126-158)."""
-    plan = _ss_plan(y, n)
     dev = _device_index(device)
-    nat = native_plan(plan, FilterPlan(), y.angles.full_turn, dev)
+    nat = _ss_plan(y, n, dev)
     rows = torch.from_numpy(np.ascontiguousarray(y.data, dtype=np.float32)).to(f"cuda:{dev}")
     img = torch.empty((n, n), dtype=torch.float32, device=f"cuda:{dev}")
     with torch.cuda.device(dev):
@@ -76,9 +65,8 @@ def forward_project(image: ImageGrid, detector: DetectorAxis, angles: AngleAxis,
     """Line integrals of ``image`` on the (t, theta) grid (projector.py:94-123);
     ``workers`` is accepted and ignored."""
     y0 = Sinogram(detector, angles, np.zeros((angles.n_theta, detector.n_t)))
-    plan = _ss_plan(y0, image.n)
     dev = _device_index(device)
-    nat = native_plan(plan, FilterPlan(), angles.full_turn, dev)
+    nat = _ss_plan(y0, image.n, dev)
     img = torch.from_numpy(np.ascontiguousarray(image.data, dtype=np.float32)).to(f"cuda:{dev}")
     out = torch.empty((angles.n_theta, detector.n_t), dtype=torch.float32, device=f"cuda:{dev}")
     with torch.cuda.device(dev):

@@ -30,7 +30,7 @@ int main(void) {
     fprintf(stderr, "ABI version mismatch\n");
     return 1;
   }
-  tb_plan_desc d = {n, V, 2, 0, 10.0, 0.1, 1, TB_INTERP_BILINEAR, 0, 0, TB_FILTER_RAMP, 1.0};
+  tb_plan_desc d = {n, V, 2, 0, 10.0, 0.1, 1, TB_INTERP_BILINEAR, 0, 0, TB_FILTER_RAMP, 1.0, 0, 0};
   tb_plan* plan = NULL;
   CHECK(tb_plan_create(&d, 0, &plan));
   size_t ws_bytes = 0;

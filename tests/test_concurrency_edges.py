@@ -85,3 +85,65 @@ def test_plain_gather_path_matches_texture_path():
     plain = F.fbp_volume(vol, plan, batch=40)  # 81960 rows: plain loads
     rel = (torch.linalg.norm(tex - plain) / torch.linalg.norm(tex)).item()
     assert rel < 5e-6, rel
+
+
+def test_odd_full_turn_bst_raises_value_error_and_ss_works():
+    """Full-turn input with an odd angle count: the reference's BST path
+    rejects it with ValueError (fourier_bp.py:331-332, 446-448); its slant
+    stack handles any count (projector.py:126-158)."""
+    import numpy as np
+    from oracle import bst_oracle as O
+    from paper_1704_08364_b200 import projector
+    from paper_1704_08364_b200.slices import AngleAxis, DetectorAxis, Sinogram
+    F = _F()
+    rng = np.random.default_rng(3)
+    n_t, A = 64, 63
+    data = O.ellipse_sinogram(O.SHEPP_LOGAN, n_t, A, full_turn=True) + rng.normal(0, 0.01, (A, n_t))
+    y = Sinogram(DetectorAxis(n_t), AngleAxis(A, full_turn=True), data)
+    with pytest.raises(ValueError):
+        F.fbp(y)
+    with pytest.raises(ValueError):
+        F.fbp(y, F.BstPlan(n_t, A // 2))
+    with pytest.raises(ValueError):
+        F.bst_backproject(y, F.BstPlan(n_t, A // 2))
+    got = F.fbp(y, F.BstPlan(n_t, A // 2), kernel="ss").data
+    ref = O.fbp(data, O.OraclePlan(n_t, A // 2), "ss", full_turn=True)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
+    bp = projector.backproject_ss(y, 48).data
+    ref2 = O.backproject_ss(data, 48, full_turn=True)
+    assert np.linalg.norm(bp - ref2) / np.linalg.norm(ref2) < 1e-5
+
+
+def test_table_free_plan_rejects_bst_calls():
+    F = _F()
+    nat = F.aux_plan(64, 64)
+    sino = torch.zeros((1, 64, 64), device="cuda")
+    img = torch.empty((1, 64, 64), device="cuda")
+    ws = nat.new_workspace(1)
+    with pytest.raises(ValueError, match="gridding tables"):
+        nat.run("fbp", sino, img, 1, 1, ws)
+
+
+def test_plan_dropped_with_work_in_flight():
+    """fbp_volume(check=False) returns with kernels queued; dropping the last
+    reference to its plan destroys it, which must wait for those kernels
+    (tb_plan_destroy drains the device) -- the result stays exact."""
+    import gc
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    vol = phantom.ellipsoid_volume(8, 256, 256, device="cuda")
+    ref = F.fbp_volume(vol, F.BstPlan(256, 256))
+    for _ in range(3):
+        out = F.fbp_volume(vol, F.BstPlan(256, 256), check=False)  # plan=None path builds a fresh plan
+        gc.collect()
+        assert torch.equal(out, ref)
+
+
+def test_backproject_stage_scale_rides_in_the_kernel():
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    vol = phantom.ellipsoid_volume(2, 128, 128, device="cuda")
+    plan = F.BstPlan(128, 128)
+    raw = F.fbp_volume(vol, plan, kernel="none")
+    scaled = F.fbp_volume(vol, plan, kernel="none", scale=F.FBP_SCALE)
+    assert torch.allclose(scaled, raw * F.FBP_SCALE, rtol=2e-6, atol=1e-7)

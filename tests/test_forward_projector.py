@@ -99,8 +99,7 @@ def test_gpu_forward_batched_linearity_1024():
     from paper_1704_08364_b200.projector import _ss_plan
     from paper_1704_08364_b200.slices import AngleAxis, DetectorAxis, Sinogram
     n, n_t, v = 1024, 1024, 128
-    plan = _ss_plan(Sinogram(DetectorAxis(n_t), AngleAxis(v), np.zeros((v, n_t))), n)
-    nat = F.native_plan(plan, F.FilterPlan(), False, 0)
+    nat = _ss_plan(Sinogram(DetectorAxis(n_t), AngleAxis(v), np.zeros((v, n_t))), n, 0)
     g = torch.Generator("cuda").manual_seed(1)
     imgs = torch.randn((3, n, n), device="cuda", generator=g)
     out = torch.empty((3, v, n_t), device="cuda")

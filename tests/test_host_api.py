@@ -74,3 +74,26 @@ def test_slab_split_covers_volume():
 def test_default_batch():
     assert default_batch(BstPlan(2048, 2048)) >= 1
     assert default_batch(BstPlan(256, 256)) > default_batch(BstPlan(1024, 1024))
+
+
+@pytest.mark.parametrize("out,msg", [
+    ("torch.empty((2, 8, 8))", "shape"),
+    ("torch.empty((3, 8, 8), dtype=torch.float64)", "float32"),
+    ("torch.empty((3, 8, 16))[:, :, ::2]", "contiguous"),
+    ("[[0.0]]", "torch.Tensor"),
+])
+def test_fbp_volume_rejects_bad_out_before_any_device_work(out, msg):
+    """The kernels write through a raw pointer: a wrong out must raise
+    ValueError up front (no device needed to see it)."""
+    import torch
+    from paper_1704_08364_b200.fourier_bp import fbp_volume
+    sino = torch.zeros((3, 8, 8))
+    with pytest.raises(ValueError, match=msg):
+        fbp_volume(sino, BstPlan(8, 8), out=eval(out))
+
+
+def test_fbp_volume_scale_only_for_unfiltered_kernel():
+    import torch
+    from paper_1704_08364_b200.fourier_bp import fbp_volume
+    with pytest.raises(ValueError, match="scale"):
+        fbp_volume(torch.zeros((1, 8, 8)), BstPlan(8, 8), kernel="bst", scale=2.0)

@@ -14,7 +14,7 @@ def test_library_loads_and_exports_every_header_symbol():
     assert len(names) >= 14
     for name in names:
         assert hasattr(lib, name), name
-    assert lib.tb_abi_version() == 1
+    assert lib.tb_abi_version() == 2
 
 
 def _desc(**kw):
@@ -38,6 +38,8 @@ def _desc(**kw):
     ({"output_n": 1025}, "output_n must be in [1, radial_samples]"),
     ({"filter_kind": 5}, "unknown filter kind"),
     ({"rolloff": 0.0}, "rolloff must be in (0, 1]"),
+    ({"n_angles": -1}, "n_angles must be >= 0"),
+    ({"flags": 6}, "unknown plan flags"),
 ])
 def test_plan_validation_mirrors_reference(kw, msg):
     lib = _native.lib()
