@@ -222,10 +222,18 @@ struct GroupSync {
   }
 };
 
-// One Stockham pass.  tw[j] = exp(-2 pi i j / N) for j < N (fp32).
-template <int N, int PASS, bool INV, class Sync = CtaSync, int RP = default_rpt(N)>
+// Offset of pass PASS's entries in a per-pass twiddle table (fft_mod):
+// passes 1.. hold ns(p) entries each.
+template <class S>
+__host__ __device__ constexpr int mod_offset(int p) { return p <= 1 ? 0 : mod_offset<S>(p - 1) + S::ns(p - 1); }
+
+// One Stockham pass.  tw[j] = exp(-2 pi i j / N) for j < N (fp32).  MOD:
+// pass p >= 1 takes its twiddle base from twm[mod_offset(p) + k] instead
+// (tables with a per-pass rotation folded in, see fft_mod).
+template <int N, int PASS, bool INV, class Sync = CtaSync, int RP = default_rpt(N), bool MOD = false>
 __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
-                                         const float2* __restrict__ tw, Sync sync = Sync()) {
+                                         const float2* __restrict__ tw, Sync sync = Sync(),
+                                         const float2* __restrict__ twm = nullptr) {
   using S = FftShape<N, RP>;
   constexpr int R = S::radix(PASS);
   constexpr int NS = S::ns(PASS);
@@ -256,7 +264,11 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
     const int j = t + b * S::TPF;
     const int k = j & (NS - 1);
     if constexpr (NS > 1) {
-      float2 w = active ? __ldg(&tw[k * (N / (NS * R))]) : make_float2(1.f, 0.f);
+      float2 w;
+      if constexpr (MOD)
+        w = active ? __ldg(&twm[mod_offset<S>(PASS) + k]) : make_float2(1.f, 0.f);
+      else
+        w = active ? __ldg(&tw[k * (N / (NS * R))]) : make_float2(1.f, 0.f);
       if (INV) w.y = -w.y;
       // powers w^m, m < R, from w, w^2, w^3 and w^{4k} (<= 3 roundings each,
       // ~10 live registers instead of R)
@@ -299,15 +311,16 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
   if constexpr (!LAST) sync();
 }
 
-template <int N, bool INV, int PASS = 0, class Sync = CtaSync, int RP = default_rpt(N)>
+template <int N, bool INV, int PASS = 0, class Sync = CtaSync, int RP = default_rpt(N), bool MOD = false>
 __device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
-                                           const float2* __restrict__ tw, Sync sync = Sync()) {
+                                           const float2* __restrict__ tw, Sync sync = Sync(),
+                                           const float2* __restrict__ twm = nullptr) {
   if constexpr (PASS < FftShape<N, RP>::NPASS) {
     // every thread runs the same instruction stream (bar.sync is .aligned:
     // no barrier may sit under a thread-divergent branch); idle threads only
     // mask their shared-memory and table traffic
-    fft_pass<N, PASS, INV, Sync, RP>(v, buf, t, active, tw, sync);
-    fft_passes<N, INV, PASS + 1, Sync, RP>(v, buf, t, active, tw, sync);
+    fft_pass<N, PASS, INV, Sync, RP, MOD>(v, buf, t, active, tw, sync, twm);
+    fft_passes<N, INV, PASS + 1, Sync, RP, MOD>(v, buf, t, active, tw, sync, twm);
   }
 }
 
@@ -318,6 +331,64 @@ template <int N, bool INV, class Sync = CtaSync, int RP = default_rpt(N)>
 __device__ __forceinline__ void fft(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
                                     const float2* __restrict__ tw, Sync sync = Sync()) {
   fft_passes<N, INV, 0, Sync, RP>(v, buf, t, active, tw, sync);
+}
+
+// Transform of a linearly modulated input without the modulation multiplies:
+// computes FFT(x[j] * exp(i alpha j)) given y[j] = x[j] * exp(i alpha N/R0 m)
+// in register slot m (the caller applies the per-slot constants of pass 0;
+// the per-thread factor exp(i alpha t) is never formed).  Writing the element
+// index e = j + m NB of pass p, the pending factor of an element read by pass
+// p is exp(i alpha (e >> 4p)), geometric in m with ratio exp(i alpha
+// stride_p) (stride_p = N / (ns(p) radix(p)), the pass's twiddle stride), so
+// it folds into the twiddle base: twm holds, for p >= 1 and k < ns(p),
+// W_N^{k stride_p} * exp(-i alpha stride_p) (forward sign; inverse passes
+// conjugate it), and the last pass leaves no factor.
+template <int N, bool INV, class Sync = CtaSync, int RP = default_rpt(N)>
+__device__ __forceinline__ void fft_mod(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
+                                        const float2* __restrict__ twm, Sync sync = Sync()) {
+  static_assert(RP == 16 || FftShape<N, RP>::NPASS == 1, "pending-factor algebra assumes radix-16 passes");
+  fft_passes<N, INV, 0, Sync, RP, true>(v, buf, t, active, nullptr, sync, twm);
+}
+
+// cos(2 pi e / 32), e in [0, 32): a switch, so a constant e folds to an
+// immediate in device code
+__host__ __device__ constexpr float cos32(int e) {
+  switch (e & 31) {
+    case 0: return 1.0f;
+    case 1: case 31: return 0.98078528040323043f;
+    case 2: case 30: return 0.92387953251128674f;
+    case 3: case 29: return 0.83146961230254524f;
+    case 4: case 28: return 0.70710678118654752f;
+    case 5: case 27: return 0.55557023301960218f;
+    case 6: case 26: return 0.38268343236508977f;
+    case 7: case 25: return 0.19509032201612826f;
+    case 8: case 24: return 0.0f;
+    case 9: case 23: return -0.19509032201612826f;
+    case 10: case 22: return -0.38268343236508977f;
+    case 11: case 21: return -0.55557023301960218f;
+    case 12: case 20: return -0.70710678118654752f;
+    case 13: case 19: return -0.83146961230254524f;
+    case 14: case 18: return -0.92387953251128674f;
+    case 15: case 17: return -0.98078528040323043f;
+    default: return -1.0f;
+  }
+}
+
+// v * exp(2 pi i e / 32) for an e that folds to a constant after unrolling
+// (quarter turns and odd eighths take the cheap forms)
+__device__ __forceinline__ float2 mul_e32(float2 v, int e) {
+  e &= 31;
+  if (e == 0) return v;
+  if (e == 8) return make_float2(-v.y, v.x);
+  if (e == 16) return make_float2(-v.x, -v.y);
+  if (e == 24) return make_float2(v.y, -v.x);
+  const float c = cos32(e), s = cos32(e + 24);  // sin(x) = cos(x - pi/2)
+  if ((e & 7) == 4) {
+    const float h = 0.70710678118654752f;
+    const float sc = c > 0.f ? h : -h, ss = s > 0.f ? h : -h;
+    return make_float2(sc * v.x - ss * v.y, ss * v.x + sc * v.y);
+  }
+  return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
 }
 
 }  // namespace tb

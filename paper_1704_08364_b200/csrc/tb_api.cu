@@ -481,6 +481,33 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
       }
     }
   }
+  // per-pass twiddle bases of fft_mod (fft.cuh) for the column IFFT of an
+  // n = L/2 crop, whose half-node modulation is exp(i alpha k), alpha = pi/L:
+  // pass p >= 1 (radix-16 passes, then one remainder) holds ns(p) entries
+  // W_L^{k s_p} exp(-i alpha s_p), s_p = L / (ns(p) radix(p))
+  std::vector<float2> twm;
+  {
+    int P = 0;
+    while ((1L << P) < L) ++P;
+    const int rpt = L < 16 ? (int)L : 16;
+    int lr = 0;
+    while ((1 << lr) < rpt) ++lr;
+    const int nfull = lr ? P / lr : 0, rem = lr ? 1 << (P % lr) : 1;
+    const int npass = nfull + (rem > 1 ? 1 : 0);
+    long ns = 1;
+    for (int q = 0; q < npass; ++q) {
+      const long radix = q < nfull ? rpt : rem;
+      if (q >= 1) {
+        const long stride = L / (ns * radix);
+        for (long k = 0; k < ns; ++k) {
+          const double a = -2.0 * kPi * (double)(k * stride) / L - kPi * (double)stride / L;
+          twm.push_back(make_float2((float)std::cos(a), (float)std::sin(a)));
+        }
+      }
+      ns *= radix;
+    }
+    if (twm.empty()) twm.push_back(make_float2(1.f, 0.f));
+  }
   // slant-stack angles (grids.py:85-95; projector.py:137-141)
   const int A = p->rows;
   const double span = d->full_turn ? 2.0 * kPi : kPi;
@@ -506,6 +533,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   const size_t o_rho = take(rho.size() * sizeof(float2));
   const size_t o_mod = take(modt.size() * sizeof(float2));
   const size_t o_ss = take(sscs.size() * sizeof(double2));
+  const size_t o_twm = take(twm.size() * sizeof(float2));
   std::vector<char> host(off, 0);
   auto put = [&](size_t o, const void* src, size_t bytes) { std::memcpy(host.data() + o, src, bytes); };
   put(o_twL, twL.data(), twL.size() * sizeof(float2));
@@ -517,6 +545,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   put(o_rho, rho.data(), rho.size() * sizeof(float2));
   put(o_mod, modt.data(), modt.size() * sizeof(float2));
   put(o_ss, sscs.data(), sscs.size() * sizeof(double2));
+  put(o_twm, twm.data(), twm.size() * sizeof(float2));
 
   int prev = -1;
   cudaGetDevice(&prev);
@@ -566,6 +595,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   dp.psi = reinterpret_cast<const float2*>(b + o_psi);
   dp.rho = reinterpret_cast<const float2*>(b + o_rho);
   dp.modt = reinterpret_cast<const float2*>(b + o_mod);
+  dp.twm = reinterpret_cast<const float2*>(b + o_twm);
   // per-slice K2 output padded to 128 B: slices never share a cache line
   dp.col_slice = (((size_t)((n + 3) / 4) * (H + 1) * 4 + 15) / 16) * 16;
   dp.prow = d->full_turn ? 2 * V : V + 1;

@@ -44,6 +44,8 @@ struct DevPlan {
   const float2* psi;    // [H]    exp(2 pi i f_k) / den_k
   const float2* rho;    // [H]    ref_k / den_k
   const float2* modt;   // [L]    half-node modulation (or null)
+  const float2* twm;    // per-pass twiddle bases of fft_mod for alpha = pi / L (the
+                        // half-node modulation of an n = L/2 crop), K2's column IFFT
   const double2* ss_cs; // [A]    (cos, sin) of the input angles
   const uint2* gridtab; // [(H+1)^2] first-quadrant gridding table
   // [(H+1)][L] half-plane gridding table of the half-turn bilinear path:
@@ -797,8 +799,13 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     const int V = p.n_theta;
     // M[a] M[b] with M[b] = M[t] M[TPF i]: the column factor M[a] folds into
     // the per-thread factor once per column
-    const float2 m_t = (p.has_mod && active) ? cmul(__ldg(p.modt + t), __ldg(p.modt + (as & (L - 1))))
-                                             : make_float2(1.f, 0.f);
+    // CROP_HALF with the TLD4 path: the half-node modulation M[a] M[b] is
+    // exp(i pi (a + b) / L); its per-thread part rides in the column IFFT's
+    // twiddles (fft_mod), its per-slot part is a constant 32nd root below,
+    // and M[a] multiplies the kept outputs
+    constexpr bool MODF = CROP_HALF && PATH == K2_TEX;
+    const float2 m_t = (p.has_mod && active && !MODF) ? cmul(__ldg(p.modt + t), __ldg(p.modt + (as & (L - 1))))
+                                                      : make_float2(1.f, 0.f);
 #ifndef TB_K2_NB
 #define TB_K2_NB 4
 #endif
@@ -846,7 +853,10 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       float2 val = make_float2(fmaf(u, r1v.x - r0v.x, r0v.x) + fmaf(r, cc[i].y - cc[i].x, cc[i].x),
                                fmaf(u, r1v.y - r0v.y, r0v.y));
       if (i >= RPT / 2) val.y = -val.y;  // lower half plane: conjugate of the reflection
-      if (p.has_mod) val = cmul(val, cmul(m_t, __ldg(p.modt + i * TPF)));
+      if constexpr (MODF)
+        val = mul_e32(val, i < RPT / 2 ? i : i + 16);  // exp(i pi b_signed / L) / exp(i pi t / L)
+      else if (p.has_mod)
+        val = cmul(val, cmul(m_t, __ldg(p.modt + i * TPF)));
 #if TB_K2_DIRECT
       v[i] = active ? val : make_float2(0.f, 0.f);
 #else
@@ -957,7 +967,10 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           const int pb = bs == -H ? -H : -bs;
           const float2 c0 = lattice_value(p, tab, pol, com, as, bs);
           const float2 m = lattice_value(p, tab, pol, com, pa, pb);
-          stg[i * TPF + t] = make_float2(0.5f * (c0.x + m.x), 0.5f * (c0.y - m.y));
+          float2 hv = make_float2(0.5f * (c0.x + m.x), 0.5f * (c0.y - m.y));
+          if (PATH == K2_TEX && CROP_HALF)  // fft_mod input: without M[a] M[t]
+            hv = cmul(hv, cconj(cmul(__ldg(p.modt + t), __ldg(p.modt + (as & (L - 1))))));
+          stg[i * TPF + t] = hv;
         }
       }
     }
@@ -985,7 +998,15 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       v[i] = val;
     }
   }
-  fft<L, true, Sync, RPT>(v, smem, t, active, p.tw_L, sync);
+  if constexpr (PATH == K2_TEX && CROP_HALF) {
+    fft_mod<L, true, Sync, RPT>(v, smem, t, active, p.twm, sync);
+    const float2 ma = __ldg(p.modt + (as & (L - 1)));
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      if (i < RPT / 4 || i >= 3 * RPT / 4) v[i] = cmul(v[i], ma);  // the kept rows
+  } else {
+    fft<L, true, Sync, RPT>(v, smem, t, active, p.tw_L, sync);
+  }
   if (active) {
     float2* out = w.columns + (size_t)q * p.col_slice;
 #pragma unroll
