@@ -142,6 +142,49 @@ struct Dft {
   }
 };
 
+// In-register DFT of size R whose inputs v[R/2 .. R-1] are zero (a
+// zero-padded first pass): the first radix-4 layer of R = 4B sees (x0, x1,
+// 0, 0) and costs 8 instead of 16 adds per butterfly.  Spelled out because
+// IEEE signed zeros forbid the compiler from folding x + 0 to x.
+template <int R, bool INV>
+struct DftHalf {
+  static constexpr int B = R / 4;
+  __device__ __forceinline__ static void run(float2* v) {
+    if constexpr (R < 4) {
+      Dft<R, INV>::run(v);  // R = 2: (x0, 0) -> (x0, x0); R = 1: nothing
+    } else if constexpr (R == 4) {
+      const float2 x0 = v[0], x1 = v[1], d = mul_q1<INV>(x1);
+      v[0] = cadd(x0, x1);
+      v[1] = cadd(x0, d);
+      v[2] = csub(x0, x1);
+      v[3] = csub(x0, d);
+    } else {
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) {
+        const float2 x0 = v[n2], x1 = v[B + n2];
+        const float2 d = mul_q1<INV>(x1);
+        v[n2] = cadd(x0, x1);
+        v[B + n2] = cadd(x0, d);
+        v[2 * B + n2] = csub(x0, x1);
+        v[3 * B + n2] = csub(x0, d);
+      }
+      Dft<R, INV>::twiddle_all(v);
+      float2 o[R];
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) {
+        float2 w[B];
+#pragma unroll
+        for (int n2 = 0; n2 < B; ++n2) w[n2] = v[B * k1 + n2];
+        Dft<B, INV>::run(w);
+#pragma unroll
+        for (int k2 = 0; k2 < B; ++k2) o[k1 + 4 * k2] = w[k2];
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) v[k] = o[k];
+    }
+  }
+};
+
 __device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
 // spad(i + c) for a compile-time c that is a multiple of 16: spad(i) + 17 c / 16
 // (lets every buffer access share one per-thread base + an immediate offset)
@@ -230,7 +273,8 @@ __host__ __device__ constexpr int mod_offset(int p) { return p <= 1 ? 0 : mod_of
 // One Stockham pass.  tw[j] = exp(-2 pi i j / N) for j < N (fp32).  MOD:
 // pass p >= 1 takes its twiddle base from twm[mod_offset(p) + k] instead
 // (tables with a per-pass rotation folded in, see fft_mod).
-template <int N, int PASS, bool INV, class Sync = CtaSync, int RP = default_rpt(N), bool MOD = false>
+template <int N, int PASS, bool INV, class Sync = CtaSync, int RP = default_rpt(N), bool MOD = false,
+          bool HALF = false>
 __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
                                          const float2* __restrict__ tw, Sync sync = Sync(),
                                          const float2* __restrict__ twm = nullptr) {
@@ -290,7 +334,12 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
         }
       }
     }
-    Dft<R, INV>::run(x[b]);
+    // HALF: the upper half of the input is zero; in the first pass (NS = 1,
+    // PER = 1) that is exactly x[m], m >= R/2
+    if constexpr (HALF && FIRST && PER == 1 && R >= 4)
+      DftHalf<R, INV>::run(x[b]);
+    else
+      Dft<R, INV>::run(x[b]);
     if constexpr (LAST) {
 #pragma unroll
       for (int m = 0; m < R; ++m) v[b + m * PER] = x[b][m];
@@ -311,7 +360,8 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
   if constexpr (!LAST) sync();
 }
 
-template <int N, bool INV, int PASS = 0, class Sync = CtaSync, int RP = default_rpt(N), bool MOD = false>
+template <int N, bool INV, int PASS = 0, class Sync = CtaSync, int RP = default_rpt(N), bool MOD = false,
+          bool HALF = false>
 __device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
                                            const float2* __restrict__ tw, Sync sync = Sync(),
                                            const float2* __restrict__ twm = nullptr) {
@@ -319,8 +369,8 @@ __device__ __forceinline__ void fft_passes(float2 (&v)[FftShape<N, RP>::RPT], fl
     // every thread runs the same instruction stream (bar.sync is .aligned:
     // no barrier may sit under a thread-divergent branch); idle threads only
     // mask their shared-memory and table traffic
-    fft_pass<N, PASS, INV, Sync, RP, MOD>(v, buf, t, active, tw, sync, twm);
-    fft_passes<N, INV, PASS + 1, Sync, RP, MOD>(v, buf, t, active, tw, sync, twm);
+    fft_pass<N, PASS, INV, Sync, RP, MOD, HALF>(v, buf, t, active, tw, sync, twm);
+    fft_passes<N, INV, PASS + 1, Sync, RP, MOD, HALF>(v, buf, t, active, tw, sync, twm);
   }
 }
 
@@ -331,6 +381,13 @@ template <int N, bool INV, class Sync = CtaSync, int RP = default_rpt(N)>
 __device__ __forceinline__ void fft(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
                                     const float2* __restrict__ tw, Sync sync = Sync()) {
   fft_passes<N, INV, 0, Sync, RP>(v, buf, t, active, tw, sync);
+}
+
+// fft of a zero-padded input: v[i] = 0 for i >= RPT/2 (x[j] = 0 for j >= N/2)
+template <int N, bool INV, class Sync = CtaSync, int RP = default_rpt(N)>
+__device__ __forceinline__ void fft_half(float2 (&v)[FftShape<N, RP>::RPT], float2* buf, int t, bool active,
+                                         const float2* __restrict__ tw, Sync sync = Sync()) {
+  fft_passes<N, INV, 0, Sync, RP, false, true>(v, buf, t, active, tw, sync);
 }
 
 // Transform of a linearly modulated input without the modulation multiplies:

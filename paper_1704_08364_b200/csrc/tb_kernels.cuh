@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 
       }
     }
     if constexpr (RAMP) {
-      fft<L, false>(v, buf, t, active, p.tw_np);
+      fft_half<L, false>(v, buf, t, active, p.tw_np);
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const float gk = active ? __ldg(p.ramp_g + t + i * TPF) : 0.f;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 
         v[i] = cscale(v[i], m);
       }
     }
-    fft<L, false>(v, buf, t, active, p.tw_L);
+    fft_half<L, false>(v, buf, t, active, p.tw_L);
     // exchange Z_k / Z_{L-k} through smem to separate the two real rows
     constexpr bool XALIGN = FftShape<L>::SMEM > 0 && (TPF % 16 == 0);
     if constexpr (XALIGN) {
