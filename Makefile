@@ -9,7 +9,7 @@ LIB := $(PKG)/lib/libtb_bst.so
 OBJ := $(PKG)/build
 CSRC := $(PKG)/csrc
 HDR := $(CSRC)/tb_kernels.cuh $(CSRC)/fft.cuh $(CSRC)/tb_launch.cuh include/tb_bst.h
-LS := 4 8 16 32 64 128 256 512 1024 2048 4096 8192
+LS := 4 8 16 32 64 128 256 512 1024 2048 4096 8192 16384
 INST := $(foreach l,$(LS),$(OBJ)/tb_inst_$(l).o)
 
 all: $(LIB)

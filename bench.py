@@ -105,29 +105,45 @@ def _cpu_sample(n, slices, threads):
     return dt, slices * n * n / dt
 
 
+def _cpu_reference(n, steps, warmup, threads):
+    """The reference's own CPU path on this host: the unmodified tomoblocks
+    pipeline (oracle/_ref, oracle/ref_bench.py) when installed, else the
+    oracle port.  Returns (voxels/s median, kind, sample, detail)."""
+    from oracle import ref_bench
+    if ref_bench.available():
+        rb = ref_bench.RefBench(n, threads)
+        try:
+            for _ in range(warmup):
+                rb.step(n)
+            runs = [rb.step(n) for _ in range(max(1, steps))]
+        finally:
+            rb.close()
+        value = statistics.median(r["voxels_per_s"] for r in runs)
+        return value, "reference", rb.describe(n), runs
+    slices = max(threads, 4)
+    for _ in range(warmup):
+        _cpu_sample(n, min(slices, threads), threads)
+    rates = [_cpu_sample(n, slices, threads)[1] for _ in range(max(1, steps))]
+    sample = f"{slices} of {n} slices of the {n}^3 workload per step (oracle fbp_volume, {threads} threads), extrapolated"
+    return statistics.median(rates), "port", sample, None
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import ref_bench
     n = args.size
     threads = os.cpu_count() or 1
-    slices = args.cpu_slices or max(threads, 4)
-    for _ in range(args.warmup):
-        _cpu_sample(n, min(slices, threads), threads)
-    times, rates = [], []
-    for _ in range(args.steps):
-        dt, r = _cpu_sample(n, slices, threads)
-        times.append(dt)
-        rates.append(r)
-    value = statistics.median(rates)
-    sample = f"{slices} of {n} slices of the {n}^3 workload per step (oracle fbp_volume, {threads} threads), extrapolated"
+    value, kind, sample, runs = _cpu_reference(n, args.steps, args.warmup, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * (n ** 3) / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic ellipsoid phantom)",
         "config": _workload(n),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                         "cpu": ref_bench.cpu_model(), "runs": runs},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -443,12 +459,13 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import ref_bench
+        if not args.no_e2e:
+            del host_in, host_out  # 2 x 32 GiB of pinned host memory back before the CPU run
         threads = os.cpu_count() or 1
-        slices = args.cpu_slices or max(threads, 4)
-        dt, rate = _cpu_sample(n, slices, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{slices} of {n} slices of the {n}^3 workload (oracle fbp_volume, {threads} threads, "
-                         f"{dt:.1f} s), extrapolated"}
+        rate, kind, sample, runs = _cpu_reference(n, 1, 0, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+               "cpu": ref_bench.cpu_model(), "runs": runs}
 
     if rank == 0:
         cfg = _workload(n)
@@ -463,7 +480,13 @@ def run_ours(args):
             "config": cfg,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_slice": alg[dom]},
+                         "algorithmic_bytes_per_slice": alg[dom],
+                         # every main kernel against the same HBM peak: its algorithmic bytes
+                         # over its summed device time in the profiled step
+                         "per_kernel": {k: {"algorithmic_bytes_per_slice": alg[k], "ms_per_step": stage[k],
+                                            "achieved_gbs": alg[k] * S / (stage[k] / 1e3) / 1e9,
+                                            "frac": alg[k] * S / (stage[k] / 1e3) / 1e9 / peak}
+                                        for k in ("k1_radial", "k2_columns", "k3_rows") if stage[k] > 0}},
             "path_roofline": {"algorithmic_bytes_per_volume": alg["total"] * n,
                               "achieved_gbs": alg["total"] * n / (ms_step / 1e3) / 1e9 / world,
                               "frac_per_gpu": alg["total"] * n / (ms_step / 1e3) / 1e9 / world / peak},

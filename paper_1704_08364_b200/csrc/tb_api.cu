@@ -27,7 +27,7 @@ thread_local std::string tb_g_err;
 namespace {
 
 constexpr double kPi = 3.14159265358979323846;
-constexpr int kMaxL = 8192;
+constexpr int kMaxL = 16384;
 
 int next_pow2(long n) {
   long m = 1;
@@ -159,7 +159,7 @@ int ramp_dispatch(const tb_plan* p, const float* in, float* out, int total_rows,
   case N:          \
     return tb_ramp_##N(p, in, out, total_rows, w, st);
     TB_CASE(4) TB_CASE(8) TB_CASE(16) TB_CASE(32) TB_CASE(64) TB_CASE(128) TB_CASE(256) TB_CASE(512)
-    TB_CASE(1024) TB_CASE(2048) TB_CASE(4096) TB_CASE(8192)
+    TB_CASE(1024) TB_CASE(2048) TB_CASE(4096) TB_CASE(8192) TB_CASE(16384)
 #undef TB_CASE
   }
   return fail(TB_ERR_UNSUPPORTED, "ramp length not supported on the GPU path");
@@ -343,7 +343,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   if (!(d->rolloff > 0.0 && d->rolloff <= 1.0))
     return fail(TB_ERR_INVALID, "rolloff must be in (0, 1]");
   if (!(d->kb_support > 0.0)) return fail(TB_ERR_INVALID, "kb_support must be > 0");
-  if (L > kMaxL) return fail(TB_ERR_UNSUPPORTED, "radial_samples > 8192 is not supported on the GPU path");
+  if (L > kMaxL) return fail(TB_ERR_UNSUPPORTED, "radial_samples > 16384 is not supported on the GPU path");
   const int rows_std = d->full_turn ? 2 * d->n_theta : d->n_theta;
   if (d->n_angles < 0) return fail(TB_ERR_INVALID, "n_angles must be >= 0");
   if (d->flags & ~TB_PLAN_NO_GRID) return fail(TB_ERR_INVALID, "unknown plan flags");

@@ -130,7 +130,12 @@ struct Launch {
     tb_plan worst;
     worst.S = L / 2;
     worst.n_t = L / 2;
-    const int s1 = (int)smem_k1(&worst), s1b = (int)smem_k1b(&worst);
+    int dev = 0, smax = 0;
+    TB_CUDA(cudaGetDevice(&dev));
+    TB_CUDA(cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if ((int)smem_k1(p) > smax || (int)smem_k1b(p) > smax)
+      return fail(TB_ERR_UNSUPPORTED, "the origin-window support needs more shared memory than the device has");
+    const int s1 = std::min((int)smem_k1(&worst), smax), s1b = std::min((int)smem_k1b(&worst), smax);
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
@@ -244,7 +249,7 @@ int Launch<L>::ramp_rows(const tb_plan* p, const float* in, float* out, int tota
 }
 
 // per-L entry points, defined in tb_inst.cu for each supported L
-#define TB_FOR_EACH_L(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+#define TB_FOR_EACH_L(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192) X(16384)
 #define TB_DECLARE_L(N)                                                                                    \
   int tb_configure_##N(tb_plan* p);                                                                      \
   int tb_group_##N(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp,       \

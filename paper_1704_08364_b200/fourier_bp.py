@@ -518,7 +518,10 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     """Reconstruct a sinogram volume [S][A][n_t] -> image volume [S][n][n].
 
     * CUDA tensor input: computed on that device, asynchronously on the
-      current stream; returns a CUDA tensor (``out`` may be given).
+      current stream; returns a CUDA tensor (``out`` may be given).  With
+      ``devices`` the volume is split into z-slabs over those GPUs: peer
+      copies over NVLink to each GPU, reconstruction there, peer gather
+      back into the output on the input's GPU.
     * CPU tensor / numpy input: streamed through ``devices`` (default: all
       visible GPUs) in contiguous z-slabs (pipeline.py:552-554 Q-blocks),
       with pinned async H2D / compute / D2H on three streams per device;
@@ -573,6 +576,10 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
         from .preprocess import preprocess_volume
         sino = preprocess_volume(sino, plan, full_turn, frames=frames, eps=eps, center=center, rings=rings)
         frames = None  # normalised by the preprocessing pass
+    if sino.is_cuda and devices is not None and frames is None and S:
+        devs = [_device_index(d) for d in devices]
+        if devs != [sino.device.index]:
+            return _device_volume_multi(sino, plan, fplan, op, full_turn, out, batch, devs, check, scale)
     if sino.is_cuda:
         dev = sino.device.index
         nat = native_plan(plan, fplan, full_turn, dev, grid=op != "fbp_ss")
@@ -597,6 +604,55 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     if frames is not None and op != "fbp":
         raise ValueError("host-resident counts are supported for kernel 'bst' (fused normalisation)")
     return _host_volume(sino, plan, fplan, op, full_turn, out, batch, devices, chunk, check, frames, eps, scale)
+
+
+def _device_volume_multi(sino, plan, fplan, op, full_turn, out, batch, devices, check, scale):
+    """Device-resident input on one GPU, reconstructed as contiguous z-slabs
+    on ``devices`` (pipeline.py:552-554 Q-blocks; no collective: slices are
+    independent).  Each slab is copied peer-to-peer to its GPU
+    (NVLink), reconstructed on its own stream and workspace, and gathered
+    peer-to-peer into the output on the input's GPU; a slab on the input's
+    GPU reads and writes in place.  The same device may appear more than once
+    (independent streams / workspaces on one GPU).  Asynchronous on the
+    input GPU's current stream, like the single-device call."""
+    S = sino.shape[0]
+    n = plan.output_n
+    src = sino.device.index
+    if out is None:
+        out = torch.empty((S, n, n), dtype=torch.float32, device=sino.device)
+    cur = torch.cuda.current_stream(src)
+    ready = torch.cuda.Event()
+    ready.record(cur)
+    jobs = []
+    for dev, (b, e) in zip(devices, _split(S, len(devices))):
+        if e <= b:
+            continue
+        m = e - b
+        nat = native_plan(plan, fplan, full_turn, dev, grid=op != "fbp_ss")
+        with torch.cuda.device(dev):
+            st = torch.cuda.Stream(dev)
+            st.wait_event(ready)
+            with torch.cuda.stream(st):
+                x = sino[b:e] if dev == src else sino[b:e].to(f"cuda:{dev}", non_blocking=True)
+                y = out[b:e] if dev == src else torch.empty((m, n, n), dtype=torch.float32, device=f"cuda:{dev}")
+                ws = nat.new_workspace(min(batch, m))
+                nat.reset_status(ws, st)
+                nat.run(op, x, y, m, min(batch, m), ws, st, scale=scale)
+                if dev != src:
+                    out[b:e].copy_(y, non_blocking=True)  # peer copy back to the input's GPU
+                done = torch.cuda.Event()
+                done.record(st)
+        jobs.append((nat, ws, st, done, x, y))
+    for nat, ws, st, done, x, y in jobs:
+        cur.wait_event(done)
+        # keep the slab buffers alive until the input GPU's stream has
+        # consumed them (the caching allocator reuses freed blocks per stream)
+        for t in (x, y, ws):
+            t.record_stream(st)
+    if check:
+        for nat, ws, st, *_ in jobs:
+            nat.read_status(ws, st)
+    return out
 
 
 def _check_out(out, shape, sino) -> None:

@@ -139,3 +139,17 @@ def test_fbp_stage_ss_kernel_against_oracle():
     out = P.make_fbp_stage(F.BstPlan(96, 96), kernel="ss").process(blk)
     for i, img in enumerate(out.slices):
         _assert_close(img.data, O.fbp(host[i], O.OraclePlan(96, 96), kernel="ss"))
+
+
+def test_device_resident_slabs_over_devices_0_0_bitwise():
+    """The device-resident multi-GPU path (slabs, per-slab stream and
+    workspace, gather into the output on the input's GPU) on a fake
+    two-device list: bitwise equal to the single-device call."""
+    F = _F()
+    vol = _noisy_volume(23, 256, seed=21)
+    plan = F.BstPlan(256, 256)
+    ref = F.fbp_volume(vol, plan, batch=4)
+    out = F.fbp_volume(vol, plan, batch=4, devices=[0, 0])
+    assert out.is_cuda and torch.equal(out, ref)
+    three = F.fbp_volume(vol, plan, batch=5, devices=[0, 0, 0], kernel="none", scale=0.25)
+    assert torch.equal(three, F.fbp_volume(vol, plan, batch=5, kernel="none", scale=0.25))

@@ -240,3 +240,28 @@ def test_largest_radial_length_8192_properties():
     b = F.fbp_volume(const, plan, kernel="none")[0].cpu().numpy()
     expect = 0.5 * O.OraclePlan(n_t, v).coverage()
     assert np.max(np.abs(b - expect)) <= 1e-4 * np.pi * 0.5
+
+
+def test_radial_length_16384_properties():
+    """L = 16384 (n_t = 8192: 1024-thread FFT blocks, radix-16 x 3 + radix-4):
+    linearity, the constant-sinogram identity and batch invariance (the fp64
+    oracle's L x L grids are 4 GiB each at this size)."""
+    F = _F()
+    from paper_1704_08364_b200 import phantom
+    n_t, v = 8192, 48
+    plan = F.BstPlan(n_t, v)
+    assert plan.radial_samples == 16384
+    x = phantom.ellipsoid_volume(2, n_t, v, device="cuda")
+    g = torch.Generator("cuda").manual_seed(6)
+    z = torch.randn(x.shape, device="cuda", generator=g)
+    fx = F.fbp_volume(x, plan)
+    fz = F.fbp_volume(z, plan)
+    fxz = F.fbp_volume(2.0 * x - 0.5 * z, plan)
+    lin = torch.linalg.norm(fxz - (2.0 * fx - 0.5 * fz)) / torch.linalg.norm(fxz)
+    assert lin.item() < 1e-5
+    one = F.fbp_volume(x[1:2].contiguous(), plan, batch=1)
+    assert torch.equal(one[0], fx[1])
+    const = torch.full((1, v, n_t), 0.5, device="cuda")
+    b = F.fbp_volume(const, plan, kernel="none")[0].cpu().numpy()
+    expect = 0.5 * O.OraclePlan(n_t, v).coverage()
+    assert np.max(np.abs(b - expect)) <= 1e-4 * np.pi * 0.5

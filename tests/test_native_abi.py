@@ -54,7 +54,7 @@ def test_plan_validation_mirrors_reference(kw, msg):
 def test_unsupported_size_reports_unsupported():
     lib = _native.lib()
     h = ctypes.c_void_p()
-    rc = lib.tb_plan_create(ctypes.byref(_desc(n_t=8192, n_theta=4)), 0, ctypes.byref(h))
+    rc = lib.tb_plan_create(ctypes.byref(_desc(n_t=16384, n_theta=4)), 0, ctypes.byref(h))  # L = 32768
     assert rc == _native.TB_ERR_UNSUPPORTED
 
 
