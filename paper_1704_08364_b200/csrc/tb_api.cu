@@ -53,6 +53,14 @@ size_t align_up(size_t x) { return (x + 511) & ~(size_t)511; }  // textureAlignm
 
 namespace {
 
+// fused schedule (Launch<L>::fused_pipeline): 0 off (the measured best), 1
+// K2(g) + K1(g+1), 2 K2(g) + K1(g+1) + K3(g-1); TB_FUSE selects (tuning)
+int fuse_cfg() {
+  const char* e = std::getenv("TB_FUSE");  // read per call: tests compare the schedules in one process
+  const int x = e ? std::atoi(e) : 0;
+  return (x >= 0 && x <= 2) ? x : 0;
+}
+
 // concurrent launch groups (streams) per call; TB_LANES overrides (tuning)
 int lanes_cfg() {
   static const int v = [] {
@@ -170,6 +178,8 @@ namespace {
 
 #define TB_CASE_CFG(N) case N: return tb_configure_##N(p);
 #define TB_CASE_GRP(N) case N: return tb_group_##N(p, sino, img, B, w, ramp, scale, st, ev);
+#define TB_CASE_PIPE(N) \
+  case N: return tb_pipe_##N(p, sino, img, n_slices, batch, lanes, in_stride, out_stride, scale, with_k3, st);
 
 int configure_dispatch(tb_plan* p) {
   switch (p->L) { TB_FOR_EACH_L(TB_CASE_CFG) }
@@ -180,6 +190,12 @@ int bst_dispatch(const tb_plan* p, const float* sino, float* img, int B, const W
                  cudaStream_t st, cudaEvent_t* ev = nullptr) {
   switch (p->L) { TB_FOR_EACH_L(TB_CASE_GRP) }
   return fail(TB_ERR_UNSUPPORTED, "radial_samples not supported on the GPU path");
+}
+
+int pipe_dispatch(const tb_plan* p, const float* sino, float* img, int n_slices, int batch, const Work* lanes,
+                  size_t in_stride, size_t out_stride, float scale, bool with_k3, cudaStream_t st) {
+  switch (p->L) { TB_FOR_EACH_L(TB_CASE_PIPE) }
+  return TB_ERR_UNSUPPORTED;
 }
 
 int check_exec_args(const tb_plan* p, const void* a, const void* b, int n_slices, int batch, const void* ws,
@@ -242,6 +258,23 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
   const long long in_row = frame_major ? (long long)n_slices * p->n_t : (long long)p->n_t;
   const size_t out_stride = (size_t)p->n * p->n;
   const int ngroups = (n_slices + batch - 1) / batch;
+  // the fused schedule (one stream, two workspace lanes) where it applies
+  if (!stage_ms && ramp && fuse_cfg() > 0 && lanes_cfg() >= 2 && ngroups >= 2) {
+    Work lw[2];
+    for (int l = 0; l < 2; ++l) {
+      lw[l] = work_for(p, batch, ws, l);
+      lw[l].in_slice = (long long)in_stride;
+      lw[l].in_row = in_row;
+      if (norm) {
+        lw[l].normtab = normtab;
+        lw[l].norm_eps = (float)norm->eps;
+        lw[l].norm_c = norm_c;
+      }
+    }
+    rc = pipe_dispatch(p, sino, img, n_slices, batch, lw, in_stride, out_stride, scale, fuse_cfg() == 2, st);
+    if (rc != TB_ERR_UNSUPPORTED) return rc;
+    rc = TB_OK;
+  }
   std::vector<cudaEvent_t> evs;
   if (stage_ms) {
     for (int i = 0; i < 5; ++i) stage_ms[i] = 0.0;

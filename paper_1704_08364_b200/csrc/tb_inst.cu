@@ -20,3 +20,10 @@ int TB_CAT(tb_ramp_, TB_L)(const tb_plan* p, const float* in, float* out, int to
                            cudaStream_t st) {
   return launch_ramp<TB_L>(p, in, out, total_rows, w, st);
 }
+
+int TB_CAT(tb_pipe_, TB_L)(const tb_plan* p, const float* sino, float* img, int n_slices, int batch,
+                           const Work* lanes, size_t in_stride, size_t out_stride, float scale, bool with_k3,
+                           cudaStream_t st) {
+  return Launch<TB_L>::fused_pipeline(p, sino, img, n_slices, batch, lanes, in_stride, out_stride, scale, with_k3,
+                                      st);
+}

@@ -127,12 +127,13 @@ __device__ __forceinline__ float norm_line(float I, float2 nt, float eps) {
 #ifndef TB_K1_MINB
 #define TB_K1_MINB 4
 #endif
+// one K1 block: row pairs of partial-sum group g of slice q (every thread of
+// the CTA; smem = the dynamic shared memory of smem_k1)
 template <int L, bool RAMP, bool NORM>
-__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_K1_MINB : 1)
-    k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
+__device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restrict__ sino, const Work& w, int g, int q,
+                                         float2* smem) {
   using K = KShape<L>;
   constexpr int RPT = K::RPT, TPF = K::TPF;
-  extern __shared__ float2 smem[];
   float2* buf = smem;
   float* sacc = reinterpret_cast<float*>(smem + K::BUF);
   // staging for the row pair (TMA bulk copies, TB_K1_SLOTS > 0), 16-B
@@ -143,8 +144,6 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 
   const int t = threadIdx.x;
   // blocks are exactly TPF threads once TPF >= 32: compile-time true there
   const bool active = TPF >= 32 || t < TPF;
-  const int q = blockIdx.y;
-  const int g = blockIdx.x;
   const int npairs = (p.rows + 1) >> 1;
   const int pr_begin = g * w.pairs_per_cta;
   const int pr_end = min(npairs, pr_begin + w.pairs_per_cta);
@@ -337,6 +336,13 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 
   if (bad) atomicOr(&w.status[0], 1);
   float* part = w.part + ((size_t)q * w.groups + g) * p.S;
   for (int i = t; i < p.S; i += blockDim.x) part[i] = sacc[i];
+}
+
+template <int L, bool RAMP, bool NORM>
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_K1_MINB : 1)
+    k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
+  extern __shared__ float2 smem[];
+  k1_block<L, RAMP, NORM>(p, sino, w, blockIdx.x, blockIdx.y, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1020,20 +1026,16 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
   }
 }
 
+// one K2 block: column group cg x slice group sg
 template <int L, bool CROP_HALF, int PATH>
-__global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB)
-    k2_columns(DevPlan p, Work w, int cols_per_cta, int slices_per_cta, int n_slices, int slice_fast) {
+__device__ __forceinline__ void k2_block(const DevPlan& p, const Work& w, int cg, int sg, int cols_per_cta,
+                                         int slices_per_cta, int n_slices, float2* smem) {
   using K2 = K2Shape<L>;
   constexpr int TPF = K2::TPF;
   constexpr int H = L / 2;
-  extern __shared__ float2 smem[];
   const int g = threadIdx.x / TPF;
   const int t = threadIdx.x % TPF;
   float2* buf = smem + g * K2::SMEM_PER_GROUP;
-  // CTA = a run of columns x a run of slices; slice_fast puts the slice runs
-  // on blockIdx.x so the resident CTAs share their columns' table rows
-  const int cg = slice_fast ? blockIdx.y : blockIdx.x;
-  const int sg = slice_fast ? blockIdx.x : blockIdx.y;
   const int q0 = sg * slices_per_cta;
   const int q1 = min(n_slices, q0 + slices_per_cta);
   const int c0 = cg * cols_per_cta;
@@ -1065,6 +1067,17 @@ __global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB)
       }
     }
   }
+}
+
+template <int L, bool CROP_HALF, int PATH>
+__global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB)
+    k2_columns(DevPlan p, Work w, int cols_per_cta, int slices_per_cta, int n_slices, int slice_fast) {
+  extern __shared__ float2 smem[];
+  // CTA = a run of columns x a run of slices; slice_fast puts the slice runs
+  // on blockIdx.x so the resident CTAs share their columns' table rows
+  const int cg = slice_fast ? blockIdx.y : blockIdx.x;
+  const int sg = slice_fast ? blockIdx.x : blockIdx.y;
+  k2_block<L, CROP_HALF, PATH>(p, w, cg, sg, cols_per_cta, slices_per_cta, n_slices, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1186,6 +1199,67 @@ __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 
   float chk = 0.f;
   k3_tile<L, CROP_HALF>(p, w, img + (size_t)blockIdx.y * p.n * p.n, out_scale, blockIdx.y, blockIdx.x, smem, chk);
   if (chk != 0.f) atomicOr(&w.status[1], 1);
+}
+
+// ---------------------------------------------------------------------------
+// Horizontally fused launch (one kernel, three kinds of independent CTAs):
+// K2 of launch group g, K1 of group g + 1 and K3 of group g - 1, whose
+// workspaces are disjoint (two lanes).  The idea: K2's gathers are bound by
+// TLD4 latency (~53 % issue active on its own) while K1 and K3 are FFT
+// arithmetic, so an SM holding a mix could fill K2's idle issue slots.
+// Measured at 2048^3 it does not (TB_FUSE=1: 176.9 ms, =2: 189.3 ms, per-group
+// launches 166.6 ms): each kernel's throughput is linear in its
+// resident CTAs, so sharing the SM only splits it, and the mix costs L1.
+// Kept (off by default, bitwise equal, tested) as the scaffold for kernels
+// that saturate a unit with fewer CTAs.  Block x maps to a task by
+// two nested Bresenham splits, so each kind's tasks are spread evenly over
+// the grid (and over time, as CTAs dispatch roughly in index order) and each
+// kind keeps its own task order (K2 slice-fast, K1 / K3 slice-major).
+// ---------------------------------------------------------------------------
+struct FusedArgs {
+  Work w2;                // K2 (group g)
+  int n2, kc2, spc2, B2, nsg2;
+  const float* sino1;     // K1 (group g + 1)
+  Work w1;
+  int n1, groups1;
+  Work w3;                // K3 (group g - 1)
+  float* img3;
+  float scale3;
+  int n3, tiles3;
+};
+
+// is position x of T one of the n items spread evenly over [0, T)?  idx =
+// its index if so, else the number of those items before x
+__device__ __forceinline__ bool bres_take(long long x, long long n, long long T, long long& idx) {
+  const long long a = (x * n) / T, b = ((x + 1) * n) / T;
+  idx = a;
+  return b > a;
+}
+
+#ifndef TB_KF_MINB
+#define TB_KF_MINB 4
+#endif
+template <int L, bool CROP_HALF, bool NORM>
+__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_KF_MINB : 1)
+    kf_fused(DevPlan p, FusedArgs a) {
+  static_assert(KShape<L>::THREADS == K2Shape<L>::THREADS, "fused CTAs share one block size");
+  extern __shared__ float2 smem[];
+  const long long x = blockIdx.x;
+  long long i3, i1;
+  if (bres_take(x, a.n3, (long long)a.n1 + a.n2 + a.n3, i3)) {
+    const int q = (int)(i3 / a.tiles3), tile = (int)(i3 % a.tiles3);
+    float chk = 0.f;
+    k3_tile<L, CROP_HALF>(p, a.w3, a.img3 + (size_t)q * p.n * p.n, a.scale3, q, tile, smem, chk);
+    if (chk != 0.f) atomicOr(&a.w3.status[1], 1);
+    return;
+  }
+  const long long y = x - i3;  // position among the K1 + K2 tasks
+  if (bres_take(y, a.n1, (long long)a.n1 + a.n2, i1)) {
+    k1_block<L, true, NORM>(p, a.sino1, a.w1, (int)(i1 % a.groups1), (int)(i1 / a.groups1), smem);
+    return;
+  }
+  const long long i2 = y - i1;
+  k2_block<L, CROP_HALF, K2_TEX>(p, a.w2, (int)(i2 / a.nsg2), (int)(i2 % a.nsg2), a.kc2, a.spc2, a.B2, smem);
 }
 
 // ---------------------------------------------------------------------------

@@ -142,6 +142,14 @@ struct Launch {
     TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1b));
     TB_CUDA(set_k2_smem<false>());
     TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
+    if constexpr (tb::KShape<L>::THREADS == tb::K2Shape<L>::THREADS && L >= 64) {
+      const int sf = (int)std::max({smem_k1(&worst), smem_k2(), smem_fft()});
+      const int sfm = std::min(sf, smax);
+      TB_CUDA(cudaFuncSetAttribute(tb::kf_fused<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sfm));
+      TB_CUDA(cudaFuncSetAttribute(tb::kf_fused<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sfm));
+      TB_CUDA(cudaFuncSetAttribute(tb::kf_fused<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sfm));
+      TB_CUDA(cudaFuncSetAttribute(tb::kf_fused<L, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sfm));
+    }
     if constexpr (L >= 64) {
       TB_CUDA(set_k2_smem<true>());
       TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
@@ -227,6 +235,88 @@ struct Launch {
 
   static int ramp_rows(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,
                        cudaStream_t st);
+
+  // The fused schedule on one stream, launch groups alternating between the
+  // two workspace lanes:
+  //   K1(0) K1b(0) | F(K2(0) + K1(1)) K1b(1) | F(K2(1) + K1(2) + K3(0)) K1b(2) | ... | K3(G-1)
+  // (with_k3 = false: K3(g) runs alone right after F(g)).  F(g)'s three parts
+  // touch disjoint lanes: K2(g) reads lane g&1's polar rows and writes its
+  // columns, K1(g+1) writes lane (g+1)&1's polar rows (read by K2(g-1) in the
+  // previous launch), K3(g-1) reads lane (g+1)&1's columns and coef mean
+  // (rewritten only by K2(g+1) / K1b(g+1), both after F(g) on the stream).
+  // lanes[]: the two lanes' Work with the input addressing set.  Returns
+  // TB_ERR_UNSUPPORTED (nothing enqueued) where the fused kernel does not
+  // apply; the caller then runs the per-group path.
+  static int fused_pipeline(const tb_plan* p, const float* sino, float* img, int n_slices, int batch,
+                            const Work* lanes, size_t in_stride, size_t out_stride, float scale, bool with_k3,
+                            cudaStream_t st) {
+    if constexpr (tb::KShape<L>::THREADS != tb::K2Shape<L>::THREADS || L < 64) {
+      return TB_ERR_UNSUPPORTED;
+    } else {
+      const DevPlan& dp = p->dp;
+      const bool tex = !dp.full_turn && dp.interp == 0 && lanes[0].polar_tex && lanes[1].polar_tex && dp.gridtab2;
+      if (!tex || p->npad != L || n_slices <= batch) return TB_ERR_UNSUPPORTED;
+      const bool norm = lanes[0].norm_eps > 0.f;
+      const bool half = 2 * p->n == L;
+      const int G = (n_slices + batch - 1) / batch;
+      auto nb = [&](int g) { return std::min(batch, n_slices - g * batch); };
+      const int tiles = (p->n + 3) / 4;
+      const int kc = K2::G;
+      const int ncg = (p->H + 1 + kc - 1) / kc;
+      // K1(0), K1b(0)
+      {
+        const dim3 g1(p->groups, nb(0));
+        if (norm)
+          tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, sino, lanes[0]);
+        else
+          tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, sino, lanes[0]);
+        tb::k1b_common<L><<<nb(0), K::K1B_THREADS, smem_k1b(p), st>>>(dp, lanes[0]);
+      }
+      const size_t smem = std::max({smem_k1(p), smem_k2(), smem_fft()});
+      for (int g = 0; g < G; ++g) {
+        tb::FusedArgs a{};
+        a.w2 = lanes[g & 1];
+        a.B2 = nb(g);
+        a.nsg2 = nb(g);
+        a.n2 = ncg * a.nsg2;
+        a.kc2 = kc;
+        a.spc2 = 1;
+        if (g + 1 < G) {
+          a.w1 = lanes[(g + 1) & 1];
+          a.sino1 = sino + (size_t)(g + 1) * batch * in_stride;
+          a.groups1 = p->groups;
+          a.n1 = p->groups * nb(g + 1);
+        }
+        if (with_k3 && g >= 1) {
+          a.w3 = lanes[(g - 1) & 1];
+          a.img3 = img + (size_t)(g - 1) * batch * out_stride;
+          a.scale3 = scale;
+          a.tiles3 = tiles;
+          a.n3 = tiles * nb(g - 1);
+        }
+        const unsigned blocks = (unsigned)(a.n1 + a.n2 + a.n3);
+        if (half) {
+          if (norm) tb::kf_fused<L, true, true><<<blocks, K::THREADS, smem, st>>>(dp, a);
+          else tb::kf_fused<L, true, false><<<blocks, K::THREADS, smem, st>>>(dp, a);
+        } else {
+          if (norm) tb::kf_fused<L, false, true><<<blocks, K::THREADS, smem, st>>>(dp, a);
+          else tb::kf_fused<L, false, false><<<blocks, K::THREADS, smem, st>>>(dp, a);
+        }
+        if (g + 1 < G) tb::k1b_common<L><<<nb(g + 1), K::K1B_THREADS, smem_k1b(p), st>>>(dp, lanes[(g + 1) & 1]);
+        if (!with_k3 || g == G - 1) {
+          const int g3 = g;  // K3(g) alone: every group without K3 fusion, the last group with it
+          float* im = img + (size_t)g3 * batch * out_stride;
+          const dim3 gk3(tiles, nb(g3));
+          if (half)
+            tb::k3_rows<L, true><<<gk3, K::THREADS, smem_fft(), st>>>(dp, lanes[g3 & 1], im, scale);
+          else
+            tb::k3_rows<L, false><<<gk3, K::THREADS, smem_fft(), st>>>(dp, lanes[g3 & 1], im, scale);
+        }
+      }
+      TB_CUDA(cudaGetLastError());
+      return TB_OK;
+    }
+  }
 };
 
 template <int NP>
@@ -255,5 +345,8 @@ int Launch<L>::ramp_rows(const tb_plan* p, const float* in, float* out, int tota
   int tb_group_##N(const tb_plan* p, const float* sino, float* img, int B, const Work& w, bool ramp,       \
                    float scale, cudaStream_t st, cudaEvent_t* ev);                                       \
   int tb_ramp_##N(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w,           \
+                  cudaStream_t st);                                                                      \
+  int tb_pipe_##N(const tb_plan* p, const float* sino, float* img, int n_slices, int batch,               \
+                  const Work* lanes, size_t in_stride, size_t out_stride, float scale, bool with_k3,       \
                   cudaStream_t st);
 TB_FOR_EACH_L(TB_DECLARE_L)

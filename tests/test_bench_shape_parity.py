@@ -153,3 +153,22 @@ def test_device_resident_slabs_over_devices_0_0_bitwise():
     assert out.is_cuda and torch.equal(out, ref)
     three = F.fbp_volume(vol, plan, batch=5, devices=[0, 0, 0], kernel="none", scale=0.25)
     assert torch.equal(three, F.fbp_volume(vol, plan, batch=5, kernel="none", scale=0.25))
+
+
+@pytest.mark.parametrize("N,S,batch", [(4096 // 2, 40, 12), (1024, 20, 6)])
+def test_fused_schedule_bitwise_equals_per_group_launches(N, S, batch, monkeypatch):
+    """TB_FUSE=2 (K2(g) + K1(g+1) + K3(g-1) in one grid, where it applies:
+    L = 4096 / 8192), TB_FUSE=1 (K2 + K1) and TB_FUSE=0 (separate launches
+    per group on two lanes, the default) run the same kernel bodies on the
+    same data: bitwise equal outputs, including a short last group."""
+    F = _F()
+    plan = F.BstPlan(N, N)
+    vol = _noisy_volume(S, N, seed=31)
+    outs = {}
+    for mode in ("0", "1", "2"):
+        monkeypatch.setenv("TB_FUSE", mode)
+        outs[mode] = F.fbp_volume(vol, plan, batch=batch)
+    assert torch.equal(outs["0"], outs["1"]) and torch.equal(outs["0"], outs["2"])
+    if N == 2048:
+        ref = O.fbp(vol[S - 1].cpu().numpy().astype(np.float64), O.OraclePlan(N, N))
+        _assert_close(outs["2"][S - 1].cpu().numpy(), ref)
