@@ -1015,13 +1015,25 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
   }
   if (active) {
     float2* out = w.columns + (size_t)q * p.col_slice;
+    if constexpr (CROP_HALF) {
+      // n = L/2: the kept rows are i < RPT/4 (m2 = t + i TPF + L/4) and
+      // i >= 3 RPT/4 (m2 = t + (i - 3 RPT/4) TPF); m2 = t + c_i with c_i a
+      // multiple of 4, so col_index is one per-thread base plus a
+      // compile-time tile offset (the other slots are DCE'd)
+      float2* ob = out + (((size_t)(t >> 2) * (H + 1) + a) * 4 + (t & 3));
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int idx = t + i * TPF;
-      const int m2 = (idx + p.n_half) & (L - 1);
-      // n = L/2: the kept rows are i < RPT/4 or i >= 3 RPT/4 (others DCE'd)
-      const bool keep = CROP_HALF ? (i < RPT / 4 || i >= 3 * RPT / 4) : (m2 < p.n);
-      if (keep) out[col_index(H, m2, a)] = v[i];
+      for (int i = 0; i < RPT; ++i) {
+        if (i < RPT / 4 || i >= 3 * RPT / 4) {
+          const int c = i < RPT / 4 ? i * TPF + L / 4 : (i - 3 * RPT / 4) * TPF;
+          ob[(size_t)(c / 4) * (H + 1) * 4] = v[i];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int m2 = (t + i * TPF + p.n_half) & (L - 1);
+        if (m2 < p.n) out[col_index(H, m2, a)] = v[i];
+      }
     }
   }
 }
