@@ -651,7 +651,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   }
   dp.gridtab2 = nullptr;
   if (p->bst_ok && !d->full_turn && d->interp == TB_INTERP_BILINEAR) {
-    const long long cnt = (long long)(H + 1) * L;
+    const long long cnt = (long long)(H + 1) * (H + 1);
     e = cudaMalloc(&p->table2, cnt * sizeof(float4));
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc(table2): ") + cudaGetErrorString(e));
     tb::build_grid_table2<<<(unsigned)((cnt + 255) / 256), 256>>>(static_cast<float4*>(p->table2), H, V, dnu, df,

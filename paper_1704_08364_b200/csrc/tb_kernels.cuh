@@ -48,10 +48,9 @@ struct DevPlan {
                         // half-node modulation of an n = L/2 crop), K2's column IFFT
   const double2* ss_cs; // [A]    (cos, sin) of the input angles
   const uint2* gridtab; // [(H+1)^2] first-quadrant gridding table
-  // [(H+1)][L] half-plane gridding table of the half-turn bilinear path:
-  // per Cartesian node (column a, row b) the texel coordinates and fp32
-  // weights of the polar sample actually read (lower half plane already
-  // reflected), or null
+  // [(H+1)][(H+1)] first-quadrant gridding table of the half-turn bilinear
+  // path: per node (a, b), a, b >= 0, the TLD4 texel coordinates (r0 + 1,
+  // t0 + 1) and the fp32 radial / angular weights, or null
   const float4* gridtab2;
   int c2pitch;          // elements per slice of Work::common2 (>= H + 1; [H..] = 0)
   int prow;             // polar rows per slice: V + 1 (half turn, row V = conj row 0) or 2V
@@ -562,11 +561,11 @@ __global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab,
   tab[i] = e;
 }
 
-// Half-plane table of the half-turn bilinear path (fourier_bp.py:222-249 per
-// node, fp64): entry [a][b] for column a in [0, H] (a = H is -L/2) and row
-// b in [0, L).  Rows b >= H (signed b < 0) are evaluated as the conjugate of
-// the point reflection (-a, -b) (upper half plane, polar rows t in [0, V],
-// row V = conj row 0), so every entry addresses rows <= V:
+// First-quadrant table of the half-turn bilinear path (fourier_bp.py:222-249
+// per node, fp64): entry [a][b] for a, b in [0, H] (angle in [0, pi/2], polar
+// rows t <= V/2).  K2 reads each entry for the node (a, b) and for the mirror
+// (-a, b) (angle pi - theta: row coordinate V + 1 - y, angular weights
+// swapped), the point reflection of the lower-half-plane node (a, -b):
 //   x = ra + 1   texel coordinate of the 2x2 TLD4 footprint (ra, ra + 1);
 //                H + 1 outside the disc (border texels: the gather is 0, and
 //                common2[H] = 0)
@@ -574,33 +573,20 @@ __global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab,
 //   z, w = rf, tf  bilinear fractions, fp64-computed, rounded to fp32
 __global__ void __launch_bounds__(256) build_grid_table2(float4* __restrict__ tab, int H, int V, double dnu,
                                                          double df, double tscale) {
-  const int L = 2 * H;
-  const long long count = (long long)(H + 1) * L;
+  const long long count = (long long)(H + 1) * (H + 1);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const int a = (int)(i / L), b = (int)(i % L);
-  int ea = a < H ? a : -H, eb = b < H ? b : b - L;
-  if (eb < 0) {  // reflected: conj C(-a, -b); -(-H) is the same node (magnitude H)
-    ea = -ea;
-    eb = -eb;
-  }
-  const double nu1 = ((double)ea * (1.0 / L)) * L * dnu;
-  const double nu2 = ((double)eb * (1.0 / L)) * L * dnu;
+  const int a = (int)(i / (H + 1)), b = (int)(i % (H + 1));
+  const int L = 2 * H;
+  const double nu1 = ((double)a * (1.0 / L)) * L * dnu;
+  const double nu2 = ((double)b * (1.0 / L)) * L * dnu;
   const double ri = hypot(nu1, nu2) / df;
-  double ph = atan2(nu2, nu1);
-  if (ph < 0.0) ph += 2.0 * 3.14159265358979323846;  // np.mod(., 2 pi); nu2 >= 0 here
-  const double ti = ph * tscale;
+  const double ti = atan2(nu2, nu1) * tscale;  // angle in [0, pi/2]
   float4 e;
   if (ri <= (double)(H - 1)) {
     const double rfl = floor(ri);
-    double tfl = floor(ti);
-    double tf = ti - tfl;
-    int t0 = (int)tfl;
-    if (t0 >= V) {  // angle pi (t0 = V, tf = 0): read it as row V with weight 1 from row V - 1
-      tf += (double)(t0 - (V - 1));
-      t0 = V - 1;
-    }
-    e = make_float4((float)(rfl + 1.0), (float)(t0 + 1), (float)(ri - rfl), (float)tf);
+    const double tfl = floor(ti);
+    e = make_float4((float)(rfl + 1.0), (float)(tfl + 1.0), (float)(ri - rfl), (float)(ti - tfl));
   } else {
     e = make_float4((float)(H + 1), 1.f, 0.f, 0.f);
   }
@@ -733,13 +719,13 @@ __device__ __forceinline__ float4 ld_table4(const float4* p) {
 // sweeping a contiguous run of columns G at a time.  Adjacent columns read
 // nearly the same polar lines, so the SM's L1 keeps the shared footprint of
 // the G concurrent columns and of the next step resident.
-#ifndef TB_K2_DIRECT
-// K2_TEX: gathered nodes straight into the FFT registers (1) or staged in
-// the FFT buffer first (0)
-#define TB_K2_DIRECT 0
-#endif
 #ifndef TB_K2_RPT
 #define TB_K2_RPT 16
+#endif
+// A/B instrumentation only (results are wrong when set): 1 = no gather, 2 = no column
+// transform, 3 = one TLD4 per node (real part reused), 4 = 3 without the transform
+#ifndef TB_K2_DBG
+#define TB_K2_DBG 0
 #endif
 template <int L>
 struct K2Shape {
@@ -816,75 +802,96 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
 #define TB_K2_NB 4
 #endif
     constexpr int NB = TB_K2_NB < RPT ? TB_K2_NB : RPT;
-    if constexpr (PATH == K2_TEX) {
-    // three-stage software pipeline over groups of NP nodes: half-plane
-    // table entries (16 B, coalesced) AH + 1 groups ahead, two TLD4 gathers
-    // plus the common-row pair AH groups ahead, bilinear of this group.
-    // Every entry already names the polar texels of the node actually read
-    // (reflection resolved at plan time), so a node costs one table load, a
-    // slice offset, two gathers, one common-row load and the interpolation;
-    // nodes outside the disc read border texels (0) and common2[H] (0)
-    // measured at 2048^3 (K2 ms, slice-fast grid): (NP, AH) = (1, 2) 87.1,
-    // (2, 1) 91.3, (2, 2) 89.8, (4, 1) 90.4; gathering straight into the FFT
-    // registers instead of staging: (1, 2) 99.4, (2, 1) 101.2 (64 registers)
-#ifdef TB_K2_NP
-    constexpr int NP0 = TB_K2_NP;
-#else
-    constexpr int NP0 = 1;
-#endif
+    if constexpr (PATH == K2_TEX && TB_K2_DBG == 1) {
+      // A/B only: no gather (time the column transform alone)
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) if (active) stg[i * TPF + t] = make_float2((float)i, (float)t);
+    } else if constexpr (PATH == K2_TEX) {
+    // Mirrored-pair gather over the first-quadrant table.  Entry b' = t +
+    // TPF j of column a drives two nodes: the direct node (a, b') and the
+    // lower-half-plane node b = L - b', whose point reflection (-a, b') is
+    // the entry's mirror about the k2 axis: angle pi - theta, i.e. texel row
+    // V + 1 - y with the angular weights swapped, same radius (same common
+    // row pair).  So one table load and one common-row load serve two nodes.
+    // The mirror node lands in slot RPT-1-j of thread TPF - t (thread 0's
+    // first mirror is b' = H instead: b' = 0 has no mirror and b = H no
+    // direct node), so a barrier precedes the reload.
+    // Software pipeline over the RPT nodes d0, m0, d1, m1, ...: TLD4 gathers
+    // AH nodes ahead, the table entry of a pair before its first gather.
+    // Nodes outside the disc read border texels (0) and common2[H] (0).
 #ifdef TB_K2_AHEAD
     constexpr int AH = TB_K2_AHEAD;
 #else
     constexpr int AH = 2;
 #endif
-    constexpr int NP = NP0 < RPT ? NP0 : RPT, NG = RPT / NP;
-    const float4* trow2 = p.gridtab2 + (size_t)a * L + t;
+    constexpr int NJ = RPT / 2;
+    const float4* qrow = p.gridtab2 + (size_t)a * (H + 1);
     const float fyoff = (float)(q * (V + 1));
-    float4 e[RPT];
+    const float fymir = fyoff + (float)(V + 1);
+    const int mb0 = t == 0 ? H : L - t;  // staging index of pair 0's mirror node
+    // per-slot part of the half-node modulation (fft_mod input): slot s holds
+    // b = t + TPF s, b_signed = b - L for s >= RPT/2: exp(i pi TPF s / L) =
+    // exp(2 pi i (16 s / RPT) / 32), times -1 in the lower half
+    auto slot_e = [](int s) { return 16 * s / RPT + (s >= RPT / 2 ? 16 : 0); };
+    const float2 ma = (!MODF && p.has_mod) ? __ldg(p.modt + (as & (L - 1))) : make_float2(1.f, 0.f);
+    float4 e[NJ];
+    float4 em0;
     float4 fre[RPT], fim[RPT];
-    float2 cc[RPT];
-    auto tload = [&](int i) { e[i] = ld_table4(trow2 + i * TPF); };
-    auto fetch = [&](int i) {
-      fre[i] = tex2Dgather<float4>(w.polar_tex, e[i].x, e[i].y + fyoff, 0);
-      fim[i] = tex2Dgather<float4>(w.polar_tex, e[i].x, e[i].y + fyoff, 1);
-      cc[i] = __ldg(com2 + ((int)e[i].x - 1));
+    float2 cc[NJ], ccm0;
+    auto tload = [&](int j) {
+      e[j] = ld_table4(qrow + t + j * TPF);
+      if (j == 0) em0 = t == 0 ? ld_table4(qrow + H) : e[0];
     };
-    auto consume = [&](int i) {
-      const float r = e[i].z, u = e[i].w;
-      const float4 re = fre[i], im = fim[i];
+    auto entry = [&](int k) { return k == 1 ? em0 : e[k >> 1]; };
+    auto fetch = [&](int k) {
+      const float4 d = entry(k);
+      const float y = (k & 1) ? fymir - d.y : d.y + fyoff;
+      fre[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 0);
+      if (TB_K2_DBG == 3 || TB_K2_DBG == 4) fim[k] = fre[k];
+      else fim[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 1);
+      if ((k & 1) == 0) cc[k >> 1] = __ldg(com2 + ((int)d.x - 1));
+      if (k == 1) ccm0 = __ldg(com2 + ((int)d.x - 1));
+    };
+    auto consume = [&](int k) {
+      const int j = k >> 1;
+      const bool mir = k & 1;
+      const float4 d = entry(k);
+      const float2 c = k == 1 ? ccm0 : cc[j];
+      const float r = d.z, u = d.w;
+      const float4 re = fre[k], im = fim[k];
       const float2 p00 = make_float2(re.w, im.w), p01 = make_float2(re.z, im.z);
       const float2 p10 = make_float2(re.x, im.x), p11 = make_float2(re.y, im.y);
       const float2 r0v = make_float2(fmaf(r, p01.x - p00.x, p00.x), fmaf(r, p01.y - p00.y, p00.y));
       const float2 r1v = make_float2(fmaf(r, p11.x - p10.x, p10.x), fmaf(r, p11.y - p10.y, p10.y));
-      float2 val = make_float2(fmaf(u, r1v.x - r0v.x, r0v.x) + fmaf(r, cc[i].y - cc[i].x, cc[i].x),
-                               fmaf(u, r1v.y - r0v.y, r0v.y));
-      if (i >= RPT / 2) val.y = -val.y;  // lower half plane: conjugate of the reflection
-      if constexpr (MODF)
-        val = mul_e32(val, i < RPT / 2 ? i : i + 16);  // exp(i pi b_signed / L) / exp(i pi t / L)
+      // mirror: the lower texel row carries the weight u of the entry
+      const float2 lo = mir ? r1v : r0v, hi = mir ? r0v : r1v;
+      float2 val = make_float2(fmaf(u, hi.x - lo.x, lo.x) + fmaf(r, c.y - c.x, c.x), fmaf(u, hi.y - lo.y, lo.y));
+      if (mir) val.y = -val.y;  // lower half plane: conjugate of the reflection
+      const int idx = mir ? (j == 0 ? mb0 : (L - t) - j * TPF) : t + j * TPF;
+      if constexpr (MODF)  // exp(i pi b_signed / L) / exp(i pi t_owner / L), slot j or RPT-1-j
+        val = mul_e32(val, slot_e(mir ? RPT - 1 - j : j));
       else if (p.has_mod)
-        val = cmul(val, cmul(m_t, __ldg(p.modt + i * TPF)));
-#if TB_K2_DIRECT
-      v[i] = active ? val : make_float2(0.f, 0.f);
-#else
-      if (active) stg[i * TPF + t] = val;
-#endif
+        val = cmul(val, cmul(ma, __ldg(p.modt + idx)));
+      if (active) stg[idx] = val;
     };
 #pragma unroll
-    for (int i = 0; i < (AH + 1) * NP && i < RPT; ++i) tload(i);
+    for (int j = 0; 2 * j <= AH && j < NJ; ++j) tload(j);
 #pragma unroll
-    for (int i = 0; i < AH * NP && i < RPT; ++i) fetch(i);
+    for (int k = 0; k < AH && k < RPT; ++k) fetch(k);
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      if (g + AH + 1 < NG) {
+    for (int g = 0; g < RPT; ++g) {
+      const int kt = g + AH + 1;
+      if (kt < RPT && (kt & 1) == 0) tload(kt >> 1);
+      if (g + AH < RPT) fetch(g + AH);
+      consume(g);
+    }
+    sync();  // mirror nodes went to other threads' slots
+    if (MODF && t == 0 && active) {
+      // thread 0 owns the mirrors of its own entries b' = TPF j (slot RPT - j,
+      // not RPT-1-j) and of b' = H (slot RPT/2): fix their slot constants
+      stg[(RPT / 2) * TPF] = mul_e32(stg[(RPT / 2) * TPF], slot_e(RPT / 2) - slot_e(RPT - 1) + 32);
 #pragma unroll
-        for (int j = 0; j < NP; ++j) tload((g + AH + 1) * NP + j);
-      }
-      if (g + AH < NG) {
-#pragma unroll
-        for (int j = 0; j < NP; ++j) fetch((g + AH) * NP + j);
-      }
-#pragma unroll
-      for (int j = 0; j < NP; ++j) consume(g * NP + j);
+      for (int i = RPT / 2 + 1; i < RPT; ++i) stg[i * TPF] = mul_e32(stg[i * TPF], slot_e(i) - slot_e(i - 1));
     }
     } else {  // plain-load gathers (no texture view: too many rows, or TB_NOTEX)
     uint2 en[NB];
@@ -954,13 +961,6 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       }
     }
     }
-#if TB_K2_DIRECT
-    if (PATH == K2_TEX && p.nyq && active) {
-      // the Nyquist fix-up below works on the (thread-private) staging slots
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) stg[i * TPF + t] = v[i];
-    }
-#endif
     if (p.nyq && active) {
       // Nyquist lines: Hermitian part 0.5 (C[k] + conj C[-k mod L]) of the fully
       // modulated lattice (.real of ifft2, fourier_bp.py:431)
@@ -980,11 +980,9 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
         }
       }
     }
-    if (PATH != K2_TEX || !TB_K2_DIRECT || p.nyq) {
 #pragma unroll
-      for (int i = 0; i < RPT; ++i) v[i] = active ? stg[i * TPF + t] : make_float2(0.f, 0.f);
-      sync();  // every thread holds its nodes before the FFT rewrites the buffer
-    }
+    for (int i = 0; i < RPT; ++i) v[i] = active ? stg[i * TPF + t] : make_float2(0.f, 0.f);
+    sync();  // every thread holds its nodes before the FFT rewrites the buffer
   } else {
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -1005,7 +1003,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     }
   }
   if constexpr (PATH == K2_TEX && CROP_HALF) {
-    fft_mod<L, true, Sync, RPT>(v, smem, t, active, p.twm, sync);
+    if (TB_K2_DBG != 2 && TB_K2_DBG != 4) fft_mod<L, true, Sync, RPT>(v, smem, t, active, p.twm, sync);
     const float2 ma = __ldg(p.modt + (as & (L - 1)));
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
