@@ -650,15 +650,20 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
     dp.gridtab = static_cast<const uint2*>(p->table);
   }
   dp.gridtab2 = nullptr;
+  dp.colext = nullptr;
   if (p->bst_ok && !d->full_turn && d->interp == TB_INTERP_BILINEAR) {
     const long long cnt = (long long)(H + 1) * (H + 1);
-    e = cudaMalloc(&p->table2, cnt * sizeof(float4));
+    // the table, then the per-column inside extents ((H + 1) ints)
+    e = cudaMalloc(&p->table2, cnt * sizeof(float4) + (size_t)(H + 1) * sizeof(int));
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc(table2): ") + cudaGetErrorString(e));
-    tb::build_grid_table2<<<(unsigned)((cnt + 255) / 256), 256>>>(static_cast<float4*>(p->table2), H, V, dnu, df,
-                                                                   (2.0 * V) / (2.0 * kPi));
+    float4* t2 = static_cast<float4*>(p->table2);
+    int* ext = reinterpret_cast<int*>(t2 + cnt);
+    tb::build_grid_table2<<<(unsigned)((cnt + 255) / 256), 256>>>(t2, H, V, dnu, df, (2.0 * V) / (2.0 * kPi));
+    tb::build_col_extent<<<(unsigned)(H + 1), 256>>>(t2, ext, H);
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("build_grid_table2: ") + cudaGetErrorString(e));
-    dp.gridtab2 = static_cast<const float4*>(p->table2);
+    dp.gridtab2 = t2;
+    dp.colext = ext;
   }
 
   int rc = configure_dispatch(p);

@@ -52,6 +52,7 @@ struct DevPlan {
   // path: per node (a, b), a, b >= 0, the TLD4 texel coordinates (r0 + 1,
   // t0 + 1) and the fp32 radial / angular weights, or null
   const float4* gridtab2;
+  const int* colext;    // [H+1] per column a: largest b' whose gridtab2 entry is inside the disc (-1: none)
   int c2pitch;          // elements per slice of Work::common2 (>= H + 1; [H..] = 0)
   int prow;             // polar rows per slice: V + 1 (half turn, row V = conj row 0) or 2V
   size_t col_slice;     // complex elements per slice of the K2 output (tiled)
@@ -592,6 +593,23 @@ __global__ void __launch_bounds__(256) build_grid_table2(float4* __restrict__ ta
   }
   tab[i] = e;
 }
+
+// Per column a of the first-quadrant table: the largest b whose node lies
+// inside the disc (x <= H), -1 if none.  One CTA per column.
+__global__ void __launch_bounds__(256) build_col_extent(const float4* __restrict__ tab, int* __restrict__ ext, int H) {
+  const int a = blockIdx.x;
+  int m = -1;
+  for (int b = threadIdx.x; b <= H; b += blockDim.x)
+    if (tab[(size_t)a * (H + 1) + b].x <= (float)H) m = max(m, b);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ int red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) m = max(m, red[i]);
+    ext[a] = max(m, red[0]);
+  }
+}
 #endif
 
 // polar sample P(t, r) of the full circle; rows t >= V of half-turn input are
@@ -723,7 +741,8 @@ __device__ __forceinline__ float4 ld_table4(const float4* p) {
 #define TB_K2_RPT 16
 #endif
 // A/B instrumentation only (results are wrong when set): 1 = no gather, 2 = no column
-// transform, 3 = one TLD4 per node (real part reused), 4 = 3 without the transform
+// transform, 3 = one TLD4 per node (real part reused), 4 = 3 without the transform,
+// 5 = every TLD4 on border texels
 #ifndef TB_K2_DBG
 #define TB_K2_DBG 0
 #endif
@@ -843,14 +862,34 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       if (j == 0) em0 = t == 0 ? ld_table4(qrow + H) : e[0];
     };
     auto entry = [&](int k) { return k == 1 ? em0 : e[k >> 1]; };
+#ifndef TB_K2_SKIP
+#define TB_K2_SKIP 2
+#endif
+    // Outside-disc skip: a TLD4 on border texels costs the TEX path nearly
+    // as much as a real one (all-border A/B: K2 67 vs 79 ms), so a warp whose
+    // 32 entries b' = (t & ~31) + lane + TPF j all lie beyond the column's
+    // inside extent (colext, largest inside b') gathers nothing and stages
+    // zeros.  The predicate is warp-uniform arithmetic (no vote).  1 =
+    // predicated TLD4s only (measured slower: 82.0 vs 78.9 ms), 2 = leave
+    // the pipeline after the warp's last live pair (78.3-78.8 ms), 0 = off.
+    const int bext = TB_K2_SKIP ? __ldg(p.colext + a) : L;
+    const int wb = t & ~31;
+    auto live = [&](int j) { return wb + j * TPF <= bext; };
     auto fetch = [&](int k) {
-      const float4 d = entry(k);
+      float4 d = entry(k);
+      if (TB_K2_DBG == 5) d.x = (float)(H + 1);  // A/B: every gather on border texels
       const float y = (k & 1) ? fymir - d.y : d.y + fyoff;
-      fre[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 0);
-      if (TB_K2_DBG == 3 || TB_K2_DBG == 4) fim[k] = fre[k];
-      else fim[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 1);
-      if ((k & 1) == 0) cc[k >> 1] = __ldg(com2 + ((int)d.x - 1));
-      if (k == 1) ccm0 = __ldg(com2 + ((int)d.x - 1));
+      if (live(k >> 1)) {
+        fre[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 0);
+        if (TB_K2_DBG == 3 || TB_K2_DBG == 4) fim[k] = fre[k];
+        else fim[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 1);
+        if ((k & 1) == 0) cc[k >> 1] = __ldg(com2 + ((int)d.x - 1));
+        if (k == 1) ccm0 = __ldg(com2 + ((int)d.x - 1));
+      } else {
+        fre[k] = fim[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((k & 1) == 0) cc[k >> 1] = make_float2(0.f, 0.f);
+        if (k == 1) ccm0 = make_float2(0.f, 0.f);
+      }
     };
     auto consume = [&](int k) {
       const int j = k >> 1;
@@ -878,13 +917,33 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     for (int j = 0; 2 * j <= AH && j < NJ; ++j) tload(j);
 #pragma unroll
     for (int k = 0; k < AH && k < RPT; ++k) fetch(k);
+#if TB_K2_SKIP == 2
+    // the warp's live pairs are j < nlive (entries increase with j): leave
+    // the pipeline after the last one (a warp-uniform branch, so the dead
+    // pairs issue no TLD4 at all) and stage zeros for the rest
+    const int nlive = bext < wb ? 0 : min(NJ, (bext - wb) / TPF + 1);
+    int jdone = NJ;
+#endif
 #pragma unroll
     for (int g = 0; g < RPT; ++g) {
       const int kt = g + AH + 1;
       if (kt < RPT && (kt & 1) == 0) tload(kt >> 1);
       if (g + AH < RPT) fetch(g + AH);
       consume(g);
+#if TB_K2_SKIP == 2
+      if ((g & 1) && g + 1 < RPT && ((g + 1) >> 1) >= nlive) {
+        jdone = (g + 1) >> 1;
+        break;
+      }
+#endif
     }
+#if TB_K2_SKIP == 2
+    if (active)
+      for (int j = jdone; j < NJ; ++j) {
+        stg[t + j * TPF] = make_float2(0.f, 0.f);
+        stg[j == 0 ? mb0 : (L - t) - j * TPF] = make_float2(0.f, 0.f);
+      }
+#endif
     sync();  // mirror nodes went to other threads' slots
     if (MODF && t == 0 && active) {
       // thread 0 owns the mirrors of its own entries b' = TPF j (slot RPT - j,
