@@ -159,6 +159,51 @@ cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
   return obj;
 }
 
+// Texture object over `rows` image rows of n floats at `ptr` (forward
+// projector), 0 when the pitch-2D view is not possible (alignment / size).
+// Cached per plan like the polar views; the cache is bounded: evicting an
+// entry waits for the device (kernels may still be reading it).
+cudaTextureObject_t image_texture(const tb_plan* p, const void* ptr, int rows) {
+  if (rows > 65000 || p->n > 65000) return 0;
+  if (const char* e = std::getenv("TB_NOTEX")) if (std::atoi(e) == 1) return 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, p->device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const size_t pitch = (size_t)p->n * sizeof(float);
+  if ((reinterpret_cast<uintptr_t>(ptr) % prop.textureAlignment) != 0 || pitch % prop.texturePitchAlignment != 0)
+    return 0;
+  std::lock_guard<std::mutex> lk(p->tex_mu);
+  for (const auto& t : p->itexs)
+    if (t.ptr == ptr && t.rows == rows) return t.obj;
+  if (p->itexs.size() >= 16) {
+    cudaDeviceSynchronize();
+    for (auto& t : p->itexs) cudaDestroyTextureObject(t.obj);
+    p->itexs.clear();
+  }
+  cudaResourceDesc res{};
+  res.resType = cudaResourceTypePitch2D;
+  res.res.pitch2D.devPtr = const_cast<void*>(ptr);
+  res.res.pitch2D.desc = cudaCreateChannelDesc<float>();
+  res.res.pitch2D.width = (size_t)p->n;
+  res.res.pitch2D.height = (size_t)rows;
+  res.res.pitch2D.pitchInBytes = pitch;
+  cudaTextureDesc td{};
+  td.addressMode[0] = cudaAddressModeBorder;  // columns -1 and n read 0 (projector.py zero padding)
+  td.addressMode[1] = cudaAddressModeClamp;   // rows outside the slice are masked in the kernel
+  td.filterMode = cudaFilterModePoint;
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  cudaTextureObject_t obj = 0;
+  if (cudaCreateTextureObject(&obj, &res, &td, nullptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  p->itexs.push_back({ptr, rows, obj});
+  return obj;
+}
+
 }  // namespace
 
 int ramp_dispatch(const tb_plan* p, const float* in, float* out, int total_rows, const Work& w, cudaStream_t st) {
@@ -686,6 +731,7 @@ int tb_plan_destroy(tb_plan* p) {
     // stream) may still read its tables and texture objects
     cudaDeviceSynchronize();
     for (auto& t : p->texs) cudaDestroyTextureObject(t.obj);
+    for (auto& t : p->itexs) cudaDestroyTextureObject(t.obj);
     cudaFree(p->blob);
     if (p->table) cudaFree(p->table);
     if (p->table2) cudaFree(p->table2);
@@ -819,7 +865,7 @@ int tb_ss(const tb_plan* p, const float* sino, float* image, int n_slices, float
   Work w{};
   w.status = nullptr;  // no workspace: the caller validates finiteness
   const int n = p->n;
-  dim3 grid((n + 15) / 16, (n + 15) / 16, 1);
+  dim3 grid((n + tb::kSsTile - 1) / tb::kSsTile, (n + tb::kSsTile - 1) / tb::kSsTile, 1);
   for (int s = 0; s < n_slices; s += 65535) {
     const int B = std::min(65535, n_slices - s);
     grid.z = B;
@@ -845,11 +891,22 @@ int tb_forward(const tb_plan* p, const float* image, float* sino, int n_slices, 
   const double h = step_length * (2.0 / p->n);
   const int m = (int)std::ceil(2.0 * std::sqrt(2.0) / h);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (int s = 0; s < n_slices; s += 65535) {
-    const int B = std::min(65535, n_slices - s);
+  const size_t nn = (size_t)p->n * p->n;
+  // bilinear: TLD4 gathers from a pitch-2D texture over runs of slices
+  // (image_texture; rows <= the pitch-2D height limit); nearest, or an
+  // image the texture unit cannot view, takes the plain-load kernel
+  const int per_tex = std::max(1, 65000 / p->n);
+  for (int s = 0; s < n_slices;) {
+    const int B = std::min(std::min(65535, per_tex), n_slices - s);
+    const float* im = image + (size_t)s * nn;
     dim3 grid((p->n_t + 127) / 128, p->rows, B);
-    tb::k6_forward<<<grid, 128, 0, st>>>(p->dp, image + (size_t)s * p->n * p->n, sino + (size_t)s * p->rows * p->n_t,
-                                          p->rows, h, m, interp == TB_INTERP_NEAREST ? 1 : 0);
+    cudaTextureObject_t tex = interp == TB_INTERP_BILINEAR ? image_texture(p, im, B * p->n) : 0;
+    if (tex)
+      tb::k6_forward_tex<<<grid, 128, 0, st>>>(p->dp, tex, sino + (size_t)s * p->rows * p->n_t, p->rows, h, m);
+    else
+      tb::k6_forward<<<grid, 128, 0, st>>>(p->dp, im, sino + (size_t)s * p->rows * p->n_t, p->rows, h, m,
+                                            interp == TB_INTERP_NEAREST ? 1 : 0);
+    s += B;
   }
   TB_CUDA(cudaGetLastError());
   return TB_OK;
@@ -933,7 +990,7 @@ int tb_fbp_ss(const tb_plan* p, const float* sino, float* image, int n_slices, i
     Work w = work_for(p, batch, ws);
     rc = ramp_dispatch(p, sino + (size_t)s0 * p->rows * p->n_t, w.filtered, B * p->rows, w, st);
     if (rc) return rc;
-    dim3 grid((n + 15) / 16, (n + 15) / 16, B);
+    dim3 grid((n + tb::kSsTile - 1) / tb::kSsTile, (n + tb::kSsTile - 1) / tb::kSsTile, B);
     tb::k5_slant<<<grid, 256, 0, st>>>(p->dp, w.filtered, p->rows, image + (size_t)s0 * n * n,
                                        (float)(1.0 / (2.0 * kPi)), w);
     TB_CUDA(cudaGetLastError());

@@ -1571,35 +1571,123 @@ __global__ void __launch_bounds__(128) k6_forward(DevPlan p, const float* __rest
   sino[((size_t)q * n_ang + j) * p.n_t + i] = (float)(acc * h);
 }
 
-__global__ void __launch_bounds__(256) k5_slant(DevPlan p, const float* __restrict__ rows, int n_ang,
-                                                float* __restrict__ img, float scale, Work w) {
-  const int m1 = blockIdx.x * 16 + (threadIdx.x & 15);
-  const int m2 = blockIdx.y * 16 + (threadIdx.x >> 4);
+// K6, texture path (bilinear; pitch-2D float texture over a run of image
+// slices, border addressing in x): one TLD4 gathers a sample's 2 x 2
+// footprint (exact fp32 pixels) instead of four scattered loads; the
+// coordinates stay fp64 as in projector.py:111-117, the footprint weights
+// are rounded to fp32 (<= 6e-8) and the sum runs in fp64.  Rows outside the
+// slice (y0 = -1 or y0 + 1 = n lie in the neighbouring slice of the
+// texture) are masked explicitly.
+__global__ void __launch_bounds__(128) k6_forward_tex(DevPlan p, cudaTextureObject_t tex, float* __restrict__ sino,
+                                                      int n_ang, double h, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
   const int q = blockIdx.z;
+  if (i >= p.n_t) return;
   const int n = p.n;
-  if (m1 >= n || m2 >= n) return;
-  const double x = -1.0 + 2.0 * ((double)m1 + 0.5) / (double)n;
-  const double y = -1.0 + 2.0 * ((double)m2 + 0.5) / (double)n;
-  const float* base = rows + (size_t)q * n_ang * p.n_t;
-  const double top = (double)(p.n_t - 1);
-  const double inv_dt = (double)p.ss_inv_dt;
-  float acc = 0.f;
-  for (int j = 0; j < n_ang; ++j) {
-    const double2 cs = __ldg(p.ss_cs + j);
-    const double fi = (fma(x, cs.x, y * cs.y) + 1.0) * inv_dt;
-    if (fi >= 0.0 && fi <= top) {
-      const double fl = floor(fi);
-      const float fr = (float)(fi - fl);
-      int i0 = (int)fl;
-      i0 = min(max(i0, 0), p.n_t - 2);
-      const float* r = base + (size_t)j * p.n_t + i0;
-      const float r0 = __ldg(r), r1 = __ldg(r + 1);
-      acc += fmaf(fr, r1 - r0, r0);
+  const double2 cs = __ldg(p.ss_cs + j);
+  const double t = -1.0 + 2.0 * (double)i / (double)(p.n_t - 1);
+  const double du = 2.0 / n, inv_du = 0.5 * n;
+  const double half = 1.4142135623730951;  // sqrt(2)
+  double lo = -half, hi = half;
+  const double lim = 1.0 + 1.5 * du;
+  auto clip = [&](double base, double dir) {
+    if (fabs(dir) < 1e-300) {
+      if (fabs(base) > lim) { lo = 1.0; hi = -1.0; }
+      return;
+    }
+    double a = (-lim - base) / dir, b = (lim - base) / dir;
+    if (a > b) { const double x = a; a = b; b = x; }
+    lo = fmax(lo, a);
+    hi = fmin(hi, b);
+  };
+  clip(t * cs.x, -cs.y);
+  clip(t * cs.y, cs.x);
+  double acc = 0.0;
+  if (hi >= lo) {
+    const int k0 = max(0, (int)floor((lo + half) / h - 0.5) - 1);
+    const int k1 = min(m - 1, (int)ceil((hi + half) / h - 0.5) + 1);
+    const float ybase = (float)(q * n + 1);
+    for (int k = k0; k <= k1; ++k) {
+      const double ell = -half + ((double)k + 0.5) * h;
+      const double fx = (t * cs.x - ell * cs.y + 1.0) * inv_du - 0.5;
+      const double fy = (t * cs.y + ell * cs.x + 1.0) * inv_du - 0.5;
+      const double x0f = floor(fx), y0f = floor(fy);
+      const int y0 = (int)y0f;
+      const float wx = (float)(fx - x0f), wy = (float)(fy - y0f);
+      // texel (x0, q n + y0) .. (x0 + 1, q n + y0 + 1)
+      const float4 g = tex2Dgather<float4>(tex, (float)(x0f + 1.0), ybase + (float)y0, 0);
+      const bool ya = y0 >= 0 && y0 < n, yb = y0 + 1 >= 0 && y0 + 1 < n;
+      const float a00 = ya ? g.w : 0.f, a01 = ya ? g.z : 0.f;
+      const float a10 = yb ? g.x : 0.f, a11 = yb ? g.y : 0.f;
+      const float r0 = fmaf(wx, a01 - a00, a00), r1 = fmaf(wx, a11 - a10, a10);
+      acc += (double)fmaf(wy, r1 - r0, r0);
     }
   }
-  const float out = acc * p.ss_weight * scale;
-  img[((size_t)q * n + m2) * n + m1] = out;
-  if (w.status && !isfinite(out)) atomicOr(&w.status[1], 1);
+  sino[((size_t)q * n_ang + j) * p.n_t + i] = (float)(acc * h);
+}
+
+// Slant stack, tiled: a CTA owns a 32 x 32 pixel tile, a thread 4 pixels of
+// one column (m2 = ty + 8 k).  The detector coordinate fi = (x c + y s + 1) /
+// dt of pixel (M1 + d1, M2 + d2) is split as fi = bi + (bf + d1 B + d2 C):
+// the tile-origin term in fp64 once per (tile, angle), rounded to an integer
+// bi plus an fp32 remainder bf, then only small fp32 offsets per pixel
+// (|remainder| < ~50 samples: 2^-18 absolute error, vs 2^-52 relative in the
+// reference), so the inner loop has no fp64.  The detector-range test and the
+// clamp follow projector.py:149-155 on fi = bi + f exactly (bi is an integer).
+constexpr int kSsTile = 32, kSsChunk = 256;
+__global__ void __launch_bounds__(256) k5_slant(DevPlan p, const float* __restrict__ rows, int n_ang,
+                                                float* __restrict__ img, float scale, Work w) {
+  __shared__ float4 ang[kSsChunk];  // (bf, B, C, bi) per angle of the chunk
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int M1 = blockIdx.x * kSsTile, M2 = blockIdx.y * kSsTile;
+  const int q = blockIdx.z;
+  const int n = p.n;
+  const float* base = rows + (size_t)q * n_ang * p.n_t;
+  const double inv_dt = (double)p.ss_inv_dt;
+  const double x0 = -1.0 + 2.0 * ((double)M1 + 0.5) / (double)n;
+  const double y0 = -1.0 + 2.0 * ((double)M2 + 0.5) / (double)n;
+  const int top = p.n_t - 1;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const float d1 = (float)tx;
+  for (int j0 = 0; j0 < n_ang; j0 += kSsChunk) {
+    const int cnt = min(kSsChunk, n_ang - j0);
+    __syncthreads();  // the previous chunk is consumed
+    for (int jj = threadIdx.x; jj < cnt; jj += blockDim.x) {
+      const double2 cs = __ldg(p.ss_cs + j0 + jj);
+      const double fi0 = (fma(x0, cs.x, y0 * cs.y) + 1.0) * inv_dt;
+      const double bi = floor(fi0);
+      ang[jj] = make_float4((float)(fi0 - bi), (float)(2.0 * cs.x / n * inv_dt), (float)(2.0 * cs.y / n * inv_dt),
+                            __int_as_float((int)bi));
+    }
+    __syncthreads();
+    for (int jj = 0; jj < cnt; ++jj) {
+      const float4 g = ang[jj];
+      const int bi = __float_as_int(g.w);
+      const float* r = base + (size_t)(j0 + jj) * p.n_t;
+      const float f0 = fmaf(d1, g.y, g.x);
+      const float lo = (float)(-bi), hi = (float)(top - bi);  // fi in [0, n_t - 1]
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float f = fmaf((float)(ty + 8 * k), g.z, f0);
+        const float fl = floorf(f);
+        const float fr = f - fl;
+        const int i0 = min(max(bi + (int)fl, 0), p.n_t - 2);
+        const float r0 = __ldg(r + i0), r1 = __ldg(r + i0 + 1);
+        acc[k] += (f >= lo && f <= hi) ? fmaf(fr, r1 - r0, r0) : 0.f;
+      }
+    }
+  }
+  const int m1 = M1 + tx;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int m2 = M2 + ty + 8 * k;
+    if (m1 < n && m2 < n) {
+      const float out = acc[k] * p.ss_weight * scale;
+      img[((size_t)q * n + m2) * n + m1] = out;
+      if (w.status && !isfinite(out)) atomicOr(&w.status[1], 1);
+    }
+  }
 }
 #endif
 

@@ -44,7 +44,7 @@ struct tb_plan {
   DevPlan dp;
   void* blob = nullptr;   // all small device tables in one allocation
   void* table = nullptr;  // gridding table [(H+1)^2] uint2
-  void* table2 = nullptr; // half-plane gridding table [(H+1)][L] float4 (half-turn bilinear)
+  void* table2 = nullptr; // first-quadrant gridding table [(H+1)][(H+1)] float4 + column extents (half-turn bilinear)
   // texture objects over workspace polar regions, keyed by (pointer, rows);
   // kept until the plan is destroyed (kernels may still be using them)
   struct Tex {
@@ -54,6 +54,7 @@ struct tb_plan {
   };
   mutable std::mutex tex_mu;
   mutable std::vector<Tex> texs;
+  mutable std::vector<Tex> itexs;  // image views of the forward projector (bounded cache)
 };
 
 // ---------------------------------------------------------------------------
