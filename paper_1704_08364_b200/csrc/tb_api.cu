@@ -128,7 +128,7 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
 // Texture object viewing `rows` polar rows of H float2 texels at `ptr`
 // (0 when the view does not fit the device's pitch-2D limits).
 cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
-  if (p->desc.full_turn || p->desc.interp != TB_INTERP_BILINEAR) return 0;
+  if (p->desc.interp != TB_INTERP_BILINEAR) return 0;
   if (rows > 65000 || p->H > 65000) return 0;
   if (const char* e = std::getenv("TB_NOTEX")) if (std::atoi(e) == 1) return 0;  // A/B: plain gathers
   std::lock_guard<std::mutex> lk(p->tex_mu);
@@ -676,7 +676,9 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   dp.twm = reinterpret_cast<const float2*>(b + o_twm);
   // per-slice K2 output padded to 128 B: slices never share a cache line
   dp.col_slice = (((size_t)((n + 3) / 4) * (H + 1) * 4 + 15) / 16) * 16;
-  dp.prow = d->full_turn ? 2 * V : V + 1;
+  // polar rows per slice: the V (2V) measured angles plus the angle-pi
+  // (angle-2 pi) mirror of row 0 that the TLD4 gathers read
+  dp.prow = d->full_turn ? 2 * V + 1 : V + 1;
   dp.c2pitch = H + 16;  // 128-B aligned rows; entries >= H are zero (outside-disc nodes)
   dp.ss_cs = reinterpret_cast<const double2*>(b + o_ss);
 
@@ -696,7 +698,7 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   }
   dp.gridtab2 = nullptr;
   dp.colext = nullptr;
-  if (p->bst_ok && !d->full_turn && d->interp == TB_INTERP_BILINEAR) {
+  if (p->bst_ok && d->interp == TB_INTERP_BILINEAR) {
     const long long cnt = (long long)(H + 1) * (H + 1);
     // the table, then the per-column inside extents ((H + 1) ints)
     e = cudaMalloc(&p->table2, cnt * sizeof(float4) + (size_t)(H + 1) * sizeof(int));

@@ -54,7 +54,7 @@ struct DevPlan {
   const float4* gridtab2;
   const int* colext;    // [H+1] per column a: largest b' whose gridtab2 entry is inside the disc (-1: none)
   int c2pitch;          // elements per slice of Work::common2 (>= H + 1; [H..] = 0)
-  int prow;             // polar rows per slice: V + 1 (half turn, row V = conj row 0) or 2V
+  int prow;             // polar rows per slice: V + 1 (half turn, row V = conj row 0) or 2V + 1 (full turn, row 2V = row 0)
   size_t col_slice;     // complex elements per slice of the K2 output (tiled)
 };
 
@@ -297,8 +297,11 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
     bad |= !(isfinite(a0) && isfinite(a1));
     float2* out0 = w.polar + ((size_t)q * p.prow + j0) * H;
     float2* out1 = out0 + H;
-    // half turn: row V holds conj(row 0), the angle-pi mirror (fourier_bp.py:310)
-    float2* outm = (!p.full_turn && j0 == 0) ? w.polar + ((size_t)q * p.prow + p.n_theta) * H : nullptr;
+    // half turn: row V holds conj(row 0), the angle-pi mirror (fourier_bp.py:310);
+    // full turn: row 2V repeats row 0 (angle 2 pi), so the texture gathers
+    // of K2_TEXF never wrap
+    float2* outm = j0 == 0 ? w.polar + ((size_t)q * p.prow + p.rows) * H : nullptr;
+    const float mconj = p.full_turn ? 1.f : -1.f;
     if (active) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
@@ -323,7 +326,7 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
           if (k == 0) { A0 = make_float2(0.f, 0.f); A1 = A0; }
           out0[k] = A0;
           if (has1) out1[k] = A1;
-          if (outm) outm[k] = make_float2(A0.x, -A0.y);
+          if (outm) outm[k] = make_float2(A0.x, mconj * A0.y);
         }
       }
     }
@@ -784,8 +787,9 @@ struct K2Shape {
 // ptxas allocates registers for one path only):
 //   K2_TEX   half-turn bilinear, TLD4 gathers driven by the half-plane table
 //   K2_PLAIN half-turn bilinear, plain loads (polar texture view unavailable)
-//   K2_ANY   full-turn input or nearest interpolation (lattice_value)
-enum { K2_ANY = 0, K2_PLAIN = 1, K2_TEX = 2 };
+//   K2_ANY   nearest interpolation, or no texture view (lattice_value)
+//   K2_TEXF  full-turn bilinear, TLD4 gathers of both half planes
+enum { K2_ANY = 0, K2_PLAIN = 1, K2_TEX = 2, K2_TEXF = 3 };
 
 template <int L, bool CROP_HALF, int PATH, class Sync>
 __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a, int q, int t, bool active,
@@ -799,12 +803,15 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
   const float2* com = w.common + (size_t)q * H;
   const uint2* tab = p.gridtab;
   float2 v[RPT];
+  // TLD4 paths: K2_TEX (half turn), K2_TEXF (full turn)
+  constexpr bool TEXP = PATH == K2_TEX || PATH == K2_TEXF;
+  constexpr bool FULL = PATH == K2_TEXF;
   if constexpr (PATH != K2_ANY) {
-    // Half-turn bilinear fast path.  A node in the lower half plane (b < 0)
-    // is the conjugate of its point reflection (-a, -b), which lies in the
-    // upper half plane and reads polar rows t in [0, V] (row V = conj row 0):
-    // no per-corner mirror logic.  Groups of NB nodes: the table entries of
-    // the next group load while this group's corners are gathered.
+    // Bilinear fast paths.  A node in the lower half plane (b < 0) is the
+    // conjugate of its point reflection (-a, -b), which lies in the upper
+    // half plane (the lattice is Hermitian: .real of ifft2; for full-turn
+    // input the Hermitian part is formed explicitly), so no per-corner
+    // mirror logic.
     const float2* com2 = w.common2 + (size_t)q * p.c2pitch;
     const uint2* trow = tab + (size_t)a * (H + 1);
     const int V = p.n_theta;
@@ -814,7 +821,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     // exp(i pi (a + b) / L); its per-thread part rides in the column IFFT's
     // twiddles (fft_mod), its per-slot part is a constant 32nd root below,
     // and M[a] multiplies the kept outputs
-    constexpr bool MODF = CROP_HALF && PATH == K2_TEX;
+    constexpr bool MODF = CROP_HALF && TEXP;
     const float2 m_t = (p.has_mod && active && !MODF) ? cmul(__ldg(p.modt + t), __ldg(p.modt + (as & (L - 1))))
                                                       : make_float2(1.f, 0.f);
 #ifndef TB_K2_NB
@@ -825,7 +832,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       // A/B only: no gather (time the column transform alone)
 #pragma unroll
       for (int i = 0; i < RPT; ++i) if (active) stg[i * TPF + t] = make_float2((float)i, (float)t);
-    } else if constexpr (PATH == K2_TEX) {
+    } else if constexpr (TEXP) {
     // Mirrored-pair gather over the first-quadrant table.  Entry b' = t +
     // TPF j of column a drives two nodes: the direct node (a, b') and the
     // lower-half-plane node b = L - b', whose point reflection (-a, b') is
@@ -838,15 +845,21 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     // Software pipeline over the RPT nodes d0, m0, d1, m1, ...: TLD4 gathers
     // AH nodes ahead, the table entry of a pair before its first gather.
     // Nodes outside the disc read border texels (0) and common2[H] (0).
+    // Full turn (K2_TEXF): a node is the Hermitian part 0.5 (C(k) + conj
+    // C(-k)) (fourier_bp.py:431): its polar sample at angle theta and the
+    // one at theta + pi (rows y + V), and for the mirror node at pi - theta
+    // and 2 pi - theta (rows V + 1 - y and 2V + 1 - y; row 2V repeats row 0),
+    // four TLD4s per node; the common row's Hermitian part is its real part.
 #ifdef TB_K2_AHEAD
     constexpr int AH = TB_K2_AHEAD;
 #else
-    constexpr int AH = 2;
+    constexpr int AH = FULL ? 1 : 2;
 #endif
     constexpr int NJ = RPT / 2;
     const float4* qrow = p.gridtab2 + (size_t)a * (H + 1);
-    const float fyoff = (float)(q * (V + 1));
+    const float fyoff = (float)(q * p.prow);
     const float fymir = fyoff + (float)(V + 1);
+    const float fyhalf = fyoff + (float)V, fymir2 = fyoff + (float)(2 * V + 1);  // full turn
     const int mb0 = t == 0 ? H : L - t;  // staging index of pair 0's mirror node
     // per-slot part of the half-node modulation (fft_mod input): slot s holds
     // b = t + TPF s, b_signed = b - L for s >= RPT/2: exp(i pi TPF s / L) =
@@ -856,6 +869,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
     float4 e[NJ];
     float4 em0;
     float4 fre[RPT], fim[RPT];
+    float4 fre2[FULL ? RPT : 1], fim2[FULL ? RPT : 1];
     float2 cc[NJ], ccm0;
     auto tload = [&](int j) {
       e[j] = ld_table4(qrow + t + j * TPF);
@@ -883,10 +897,16 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
         fre[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 0);
         if (TB_K2_DBG == 3 || TB_K2_DBG == 4) fim[k] = fre[k];
         else fim[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 1);
+        if constexpr (FULL) {
+          const float y2 = (k & 1) ? fymir2 - d.y : d.y + fyhalf;
+          fre2[k] = tex2Dgather<float4>(w.polar_tex, d.x, y2, 0);
+          fim2[k] = tex2Dgather<float4>(w.polar_tex, d.x, y2, 1);
+        }
         if ((k & 1) == 0) cc[k >> 1] = __ldg(com2 + ((int)d.x - 1));
         if (k == 1) ccm0 = __ldg(com2 + ((int)d.x - 1));
       } else {
         fre[k] = fim[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (FULL) fre2[k] = fim2[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         if ((k & 1) == 0) cc[k >> 1] = make_float2(0.f, 0.f);
         if (k == 1) ccm0 = make_float2(0.f, 0.f);
       }
@@ -897,15 +917,27 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       const float4 d = entry(k);
       const float2 c = k == 1 ? ccm0 : cc[j];
       const float r = d.z, u = d.w;
-      const float4 re = fre[k], im = fim[k];
-      const float2 p00 = make_float2(re.w, im.w), p01 = make_float2(re.z, im.z);
-      const float2 p10 = make_float2(re.x, im.x), p11 = make_float2(re.y, im.y);
-      const float2 r0v = make_float2(fmaf(r, p01.x - p00.x, p00.x), fmaf(r, p01.y - p00.y, p00.y));
-      const float2 r1v = make_float2(fmaf(r, p11.x - p10.x, p10.x), fmaf(r, p11.y - p10.y, p10.y));
-      // mirror: the lower texel row carries the weight u of the entry
-      const float2 lo = mir ? r1v : r0v, hi = mir ? r0v : r1v;
-      float2 val = make_float2(fmaf(u, hi.x - lo.x, lo.x) + fmaf(r, c.y - c.x, c.x), fmaf(u, hi.y - lo.y, lo.y));
-      if (mir) val.y = -val.y;  // lower half plane: conjugate of the reflection
+      // bilinear value of a TLD4 pair; mirror: the lower texel row carries
+      // the weight u of the entry
+      auto bil = [&](const float4 re, const float4 im) {
+        const float2 p00 = make_float2(re.w, im.w), p01 = make_float2(re.z, im.z);
+        const float2 p10 = make_float2(re.x, im.x), p11 = make_float2(re.y, im.y);
+        const float2 r0v = make_float2(fmaf(r, p01.x - p00.x, p00.x), fmaf(r, p01.y - p00.y, p00.y));
+        const float2 r1v = make_float2(fmaf(r, p11.x - p10.x, p10.x), fmaf(r, p11.y - p10.y, p10.y));
+        const float2 lo = mir ? r1v : r0v, hi = mir ? r0v : r1v;
+        return make_float2(fmaf(u, hi.x - lo.x, lo.x), fmaf(u, hi.y - lo.y, lo.y));
+      };
+      const float2 b1 = bil(fre[k], fim[k]);
+      float2 val;
+      if constexpr (FULL) {
+        // direct: 0.5 (C(theta) + conj C(theta + pi)); mirror (conjugate of
+        // the reflection): 0.5 (conj C(pi - theta) + C(2 pi - theta))
+        const float2 b2 = bil(fre2[k], fim2[k]);
+        val = make_float2(0.5f * (b1.x + b2.x), mir ? 0.5f * (b2.y - b1.y) : 0.5f * (b1.y - b2.y));
+      } else {
+        val = mir ? cconj(b1) : b1;  // lower half plane: conjugate of the reflection
+      }
+      val.x += fmaf(r, c.y - c.x, c.x);
       const int idx = mir ? (j == 0 ? mb0 : (L - t) - j * TPF) : t + j * TPF;
       if constexpr (MODF)  // exp(i pi b_signed / L) / exp(i pi t_owner / L), slot j or RPT-1-j
         val = mul_e32(val, slot_e(mir ? RPT - 1 - j : j));
@@ -1033,7 +1065,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
           const float2 c0 = lattice_value(p, tab, pol, com, as, bs);
           const float2 m = lattice_value(p, tab, pol, com, pa, pb);
           float2 hv = make_float2(0.5f * (c0.x + m.x), 0.5f * (c0.y - m.y));
-          if (PATH == K2_TEX && CROP_HALF)  // fft_mod input: without M[a] M[t]
+          if (TEXP && CROP_HALF)  // fft_mod input: without M[a] M[t]
             hv = cmul(hv, cconj(cmul(__ldg(p.modt + t), __ldg(p.modt + (as & (L - 1))))));
           stg[i * TPF + t] = hv;
         }
@@ -1061,7 +1093,7 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       v[i] = val;
     }
   }
-  if constexpr (PATH == K2_TEX && CROP_HALF) {
+  if constexpr (TEXP && CROP_HALF) {
     if (TB_K2_DBG != 2 && TB_K2_DBG != 4) fft_mod<L, true, Sync, RPT>(v, smem, t, active, p.twm, sync);
     const float2 ma = __ldg(p.modt + (as & (L - 1)));
 #pragma unroll

@@ -110,14 +110,18 @@ struct Launch {
     cudaError_t e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_ANY>, a, (int)smem_k2());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_PLAIN>, a, (int)smem_k2());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_TEX>, a, (int)smem_k2());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_TEXF>, a, (int)smem_k2());
     return e;
   }
   template <bool CH>
   static void launch_k2(const DevPlan& dp, const Work& w, dim3 g2, cudaStream_t st, int kc, int spc, int B, int sf) {
-    if (dp.full_turn || dp.interp != 0)
-      tb::k2_columns<L, CH, tb::K2_ANY><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
-    else if (w.polar_tex && dp.gridtab2)
+    const bool tex = dp.interp == 0 && w.polar_tex && dp.gridtab2;
+    if (tex && dp.full_turn)
+      tb::k2_columns<L, CH, tb::K2_TEXF><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
+    else if (tex)
       tb::k2_columns<L, CH, tb::K2_TEX><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
+    else if (dp.full_turn || dp.interp != 0)
+      tb::k2_columns<L, CH, tb::K2_ANY><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
     else
       tb::k2_columns<L, CH, tb::K2_PLAIN><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
   }
@@ -213,7 +217,7 @@ struct Launch {
     mark(2, 1);
     const bool half = L >= 64 && 2 * p->n == L;
     mark(3, 0);
-    const bool tex = !dp.full_turn && dp.interp == 0 && w.polar_tex && dp.gridtab2;
+    const bool tex = dp.interp == 0 && w.polar_tex && dp.gridtab2;
     const int kc = k2_cols(p, tex);
     const int spc = k2_slices(B);
     const int ncg = (p->H + 1 + kc - 1) / kc, nsg = (B + spc - 1) / spc;

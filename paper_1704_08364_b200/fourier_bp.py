@@ -467,15 +467,15 @@ def fbp(y: Sinogram, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
 # ---------------------------------------------------------------------------
 
 
-def default_batch(plan: BstPlan) -> int:
+def default_batch(plan: BstPlan, full_turn: bool = False) -> int:
     """Slices per launch group (two groups in flight on two streams).  Larger
     groups fill the 148 SMs with fewer wave tails: at L = 4096 the measured
     step falls from 218 ms (4 slices) to 204 ms (24-31 slices,
     profiles/README.md).  Bounded by the polar texture's height,
-    batch * (n_theta + 1) <= 65000 rows (31 slices at 2048 angles), and at
-    64 slices."""
+    batch * polar rows <= 65000 (V + 1 rows per slice for half-turn input:
+    31 slices at 2048 angles; 2V + 1 for full turn: 15), and at 64 slices."""
     L = plan.radial_samples
-    rows = plan.n_theta + 1
+    rows = (2 * plan.n_theta if full_turn else plan.n_theta) + 1
     if L >= 1024:
         return max(1, min(64, 65000 // rows))
     return max(1, min(64, (4096 // L) ** 2, 65000 // rows))
@@ -569,7 +569,7 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
     if out is not None:
         _check_out(out, (S, n, n), sino)
     if batch is None:
-        batch = default_batch(plan)
+        batch = default_batch(plan, full_turn)
     if (center is not None or rings is not None) and not sino.is_cuda:
         raise ValueError("center / rings stages run on device-resident volumes")
     if sino.is_cuda and S and (center is not None or rings is not None):

@@ -172,3 +172,29 @@ def test_fused_schedule_bitwise_equals_per_group_launches(N, S, batch, monkeypat
     if N == 2048:
         ref = O.fbp(vol[S - 1].cpu().numpy().astype(np.float64), O.OraclePlan(N, N))
         _assert_close(outs["2"][S - 1].cpu().numpy(), ref)
+
+
+def test_full_turn_texture_path_against_oracle_and_lattice_path(monkeypatch):
+    """Full-turn input (2V rows over 2 pi) on the TLD4 path K2_TEXF: launch
+    groups of 8 on two lanes (texture rows 8 (2V + 1) per lane), slices
+    against the oracle, and the whole volume against the per-node
+    lattice_value path (TB_NOTEX=1: no texture view -> K2_ANY), whose
+    unorm16 table fractions carry up to 2^-17 weight error (measured
+    difference 3.9e-6)."""
+    F = _F()
+    N, S = 512, 20
+    plan = F.BstPlan(N, N)
+    assert F.default_batch(plan, full_turn=True) == 65000 // (2 * N + 1)
+    ell = O.ellipse_sinogram(O.SHEPP_LOGAN, N, 2 * N, full_turn=True)
+    g = torch.Generator("cuda").manual_seed(5)
+    vol = torch.from_numpy(ell.astype(np.float32)).cuda().expand(S, -1, -1).contiguous()
+    vol += 0.05 * torch.randn(vol.shape, device="cuda", generator=g)
+    out = F.fbp_volume(vol, plan, full_turn=True, batch=8)
+    op = O.OraclePlan(N, N)
+    for k in (0, 7, 8, 19):
+        ref = O.fbp(vol[k].cpu().numpy().astype(np.float64), op, full_turn=True)
+        _assert_close(out[k].cpu().numpy(), ref)
+    monkeypatch.setenv("TB_NOTEX", "1")
+    lat = F.fbp_volume(vol, plan, full_turn=True, batch=8)
+    d = (torch.linalg.norm(lat - out) / torch.linalg.norm(lat)).item()
+    assert d < 2e-5, d

@@ -111,3 +111,31 @@ def test_gpu_forward_batched_linearity_1024():
     one = torch.empty((1, v, n_t), device="cuda")
     nat.forward(imgs[2:3].contiguous(), one, 1)
     assert torch.equal(one[0], out[2])
+
+
+@pytest.mark.gpu
+def test_gpu_forward_texture_path_chunks_and_plain_fallback(monkeypatch):
+    """The bilinear forward projector reads images through pitch-2D texture
+    views of up to 65000 rows (31 slices at n = 2048): a 33-slice call spans
+    two views, and slices 30 / 31 / 32 sit on the view boundaries, whose
+    neighbouring rows must be masked.  Each slice equals the single-slice
+    call bitwise, and the plain-load kernel (TB_NOTEX=1, also the path for
+    images the texture unit cannot view) agrees to fp32 rounding."""
+    torch = _cuda()
+    from paper_1704_08364_b200.projector import _ss_plan
+    from paper_1704_08364_b200.slices import AngleAxis, DetectorAxis, Sinogram
+    n, n_t, v, S = 2048, 2048, 3, 33
+    nat = _ss_plan(Sinogram(DetectorAxis(n_t), AngleAxis(v), np.zeros((v, n_t))), n, 0)
+    g = torch.Generator("cuda").manual_seed(3)
+    imgs = torch.rand((S, n, n), device="cuda", generator=g)
+    out = torch.empty((S, v, n_t), device="cuda")
+    nat.forward(imgs, out, S)
+    for k in (0, 29, 30, 31, 32):
+        one = torch.empty((1, v, n_t), device="cuda")
+        nat.forward(imgs[k:k + 1].contiguous(), one, 1)
+        assert torch.equal(one[0], out[k]), k
+    monkeypatch.setenv("TB_NOTEX", "1")
+    plain = torch.empty((2, v, n_t), device="cuda")
+    nat.forward(imgs[30:32].contiguous(), plain, 2)
+    d = torch.linalg.norm(plain - out[30:32]) / torch.linalg.norm(out[30:32])
+    assert d.item() < 1e-6
