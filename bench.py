@@ -412,7 +412,7 @@ def run_ours(args):
         f1.record(stream)
         torch.cuda.synchronize()
         fms = f0.elapsed_time(f1)
-        fwd = {"kernel": "k6_forward (projector.forward_project, step 0.5, bilinear)", "slices_sampled": 1,
+        fwd = {"kernel": "k6_forward_tex (projector.forward_project, step 0.5, bilinear, TLD4)", "slices_sampled": 1,
                "ms_per_slice": fms, "ray_samples_per_s": n * n * math.ceil(2 * math.sqrt(2) * n) / (fms / 1e3)}
         del one
 
@@ -434,6 +434,29 @@ def run_ours(args):
               "voxels_per_s": n * n / (ss_ms / 1e3), "bst_ms_per_slice": ms_step / S,
               "bst_speedup": ss_ms / (ms_step / S)}
         nat.read_status(ws)
+
+    # the BST paths the benchmark shape does not take (nearest interpolation:
+    # K2_ANY; full-turn input, 2V rows: K2_TEXF), device-resident through the
+    # public fbp_volume on a bounded sample of slices (any data: timing only)
+    paths = None
+    if not args.no_ss and S > 0:
+        k = min(S, 31)
+        paths = {}
+        for name, interp, full in (("half_nearest", "nearest", False), ("full_turn_bilinear", "bilinear", True)):
+            pl = F.BstPlan(n, n, interp=interp)
+            src = torch.cat([sino[:k], sino[:k].flip(2)], dim=1).contiguous() if full else sino[:k]
+            o = torch.empty((k, n, n), dtype=torch.float32, device=dev)
+            with torch.cuda.stream(stream):
+                F.fbp_volume(src, pl, full_turn=full, out=o)  # warm-up (plan tables, textures)
+                torch.cuda.synchronize()
+                p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                p0.record(stream)
+                F.fbp_volume(src, pl, full_turn=full, out=o, check=False)
+                p1.record(stream)
+            torch.cuda.synchronize()
+            paths[name] = {"slices_sampled": k, "ms_per_slice": p0.elapsed_time(p1) / k,
+                           "vs_benchmark_path": p0.elapsed_time(p1) / k / (ms_step / S)}
+            del src, o, pl
 
     # end to end through the public API with pinned host buffers
     e2e = None
@@ -495,6 +518,7 @@ def run_ours(args):
             "gpu_launches": sum(launches.values()) * args.steps,
             "ss_comparator": ss,
             "forward_projector": fwd,
+            "other_paths": paths,
             "counts_path": counts_path,
             "preprocess_path": pre_path,
             "e2e": e2e,
