@@ -128,7 +128,8 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
 // Texture object viewing `rows` polar rows of H float2 texels at `ptr`
 // (0 when the view does not fit the device's pitch-2D limits).
 cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
-  if (p->desc.interp != TB_INTERP_BILINEAR) return 0;
+  // bilinear (half or full turn: K2_TEX / K2_TEXF) and half-turn nearest (K2_TEXN)
+  if (p->desc.interp != TB_INTERP_BILINEAR && p->desc.full_turn) return 0;
   if (rows > 65000 || p->H > 65000) return 0;
   if (const char* e = std::getenv("TB_NOTEX")) if (std::atoi(e) == 1) return 0;  // A/B: plain gathers
   std::lock_guard<std::mutex> lk(p->tex_mu);
@@ -698,14 +699,15 @@ int tb_plan_create(const tb_plan_desc* d, int device, tb_plan** out) {
   }
   dp.gridtab2 = nullptr;
   dp.colext = nullptr;
-  if (p->bst_ok && d->interp == TB_INTERP_BILINEAR) {
+  if (p->bst_ok && (d->interp == TB_INTERP_BILINEAR || !d->full_turn)) {
     const long long cnt = (long long)(H + 1) * (H + 1);
     // the table, then the per-column inside extents ((H + 1) ints)
     e = cudaMalloc(&p->table2, cnt * sizeof(float4) + (size_t)(H + 1) * sizeof(int));
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("cudaMalloc(table2): ") + cudaGetErrorString(e));
     float4* t2 = static_cast<float4*>(p->table2);
     int* ext = reinterpret_cast<int*>(t2 + cnt);
-    tb::build_grid_table2<<<(unsigned)((cnt + 255) / 256), 256>>>(t2, H, V, dnu, df, (2.0 * V) / (2.0 * kPi));
+    tb::build_grid_table2<<<(unsigned)((cnt + 255) / 256), 256>>>(t2, H, V, dnu, df, (2.0 * V) / (2.0 * kPi),
+                                                                   d->interp == TB_INTERP_NEAREST ? 1 : 0);
     tb::build_col_extent<<<(unsigned)(H + 1), 256>>>(t2, ext, H);
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cleanup(TB_ERR_CUDA, std::string("build_grid_table2: ") + cudaGetErrorString(e));

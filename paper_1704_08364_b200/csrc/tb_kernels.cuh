@@ -575,8 +575,12 @@ __global__ void __launch_bounds__(256) build_grid_table(uint2* __restrict__ tab,
 //                common2[H] = 0)
 //   y = t0 + 1   row coordinate within the slice's V + 1 rows
 //   z, w = rf, tf  bilinear fractions, fp64-computed, rounded to fp32
+//   nearest (K2_TEXN): x = ir + 0.5, y = it + 0.5 (texel centres, np.rint
+//   of fourier_bp.py:234-236 in fp64), z = the row of the mirror node (a, -b)
+//   as the reference rounds it (angle 2 pi - theta, minus V: the
+//   conjugated half-turn row), w = 0; x = H + 0.5 outside the disc
 __global__ void __launch_bounds__(256) build_grid_table2(float4* __restrict__ tab, int H, int V, double dnu,
-                                                         double df, double tscale) {
+                                                         double df, double tscale, int nearest) {
   const long long count = (long long)(H + 1) * (H + 1);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
@@ -587,7 +591,17 @@ __global__ void __launch_bounds__(256) build_grid_table2(float4* __restrict__ ta
   const double ri = hypot(nu1, nu2) / df;
   const double ti = atan2(nu2, nu1) * tscale;  // angle in [0, pi/2]
   float4 e;
-  if (ri <= (double)(H - 1)) {
+  if (nearest) {
+    const int ir = (int)rint(ri);
+    double pm = atan2(-nu2, nu1);  // the mirror node's own angle, np.mod(., 2 pi)
+    if (pm < 0.0) pm += 2.0 * 3.14159265358979323846;
+    int itm = (int)rint(pm * tscale) % (2 * V);
+    itm = itm == 0 ? V : itm - V;  // extended row 2V (= 0) is the conjugate of texture row V
+    if (ir <= H - 1)
+      e = make_float4((float)ir + 0.5f, (float)rint(ti) + 0.5f, (float)itm + 0.5f, 0.f);
+    else
+      e = make_float4((float)H + 0.5f, 0.5f, 0.5f, 0.f);
+  } else if (ri <= (double)(H - 1)) {
     const double rfl = floor(ri);
     const double tfl = floor(ti);
     e = make_float4((float)(rfl + 1.0), (float)(tfl + 1.0), (float)(ri - rfl), (float)(ti - tfl));
@@ -789,7 +803,8 @@ struct K2Shape {
 //   K2_PLAIN half-turn bilinear, plain loads (polar texture view unavailable)
 //   K2_ANY   nearest interpolation, or no texture view (lattice_value)
 //   K2_TEXF  full-turn bilinear, TLD4 gathers of both half planes
-enum { K2_ANY = 0, K2_PLAIN = 1, K2_TEX = 2, K2_TEXF = 3 };
+//   K2_TEXN  half-turn nearest, one point-sampled texel per node
+enum { K2_ANY = 0, K2_PLAIN = 1, K2_TEX = 2, K2_TEXF = 3, K2_TEXN = 4 };
 
 template <int L, bool CROP_HALF, int PATH, class Sync>
 __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a, int q, int t, bool active,
@@ -804,8 +819,9 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
   const uint2* tab = p.gridtab;
   float2 v[RPT];
   // TLD4 paths: K2_TEX (half turn), K2_TEXF (full turn)
-  constexpr bool TEXP = PATH == K2_TEX || PATH == K2_TEXF;
+  constexpr bool TEXP = PATH == K2_TEX || PATH == K2_TEXF || PATH == K2_TEXN;
   constexpr bool FULL = PATH == K2_TEXF;
+  constexpr bool NEAR = PATH == K2_TEXN;
   if constexpr (PATH != K2_ANY) {
     // Bilinear fast paths.  A node in the lower half plane (b < 0) is the
     // conjugate of its point reflection (-a, -b), which lies in the upper
@@ -894,16 +910,24 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       if (TB_K2_DBG == 5) d.x = (float)(H + 1);  // A/B: every gather on border texels
       const float y = (k & 1) ? fymir - d.y : d.y + fyoff;
       if (live(k >> 1)) {
-        fre[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 0);
-        if (TB_K2_DBG == 3 || TB_K2_DBG == 4) fim[k] = fre[k];
-        else fim[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 1);
+        if constexpr (NEAR) {
+          // the entry's z is the mirror's own rounded row (np.rint in fp64)
+          const float2 v = tex2D<float2>(w.polar_tex, d.x, (k & 1) ? d.z + fyoff : d.y + fyoff);
+          fre[k] = make_float4(v.x, v.y, 0.f, 0.f);
+        } else {
+          fre[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 0);
+          if (TB_K2_DBG == 3 || TB_K2_DBG == 4) fim[k] = fre[k];
+          else fim[k] = tex2Dgather<float4>(w.polar_tex, d.x, y, 1);
+        }
         if constexpr (FULL) {
           const float y2 = (k & 1) ? fymir2 - d.y : d.y + fyhalf;
           fre2[k] = tex2Dgather<float4>(w.polar_tex, d.x, y2, 0);
           fim2[k] = tex2Dgather<float4>(w.polar_tex, d.x, y2, 1);
         }
-        if ((k & 1) == 0) cc[k >> 1] = __ldg(com2 + ((int)d.x - 1));
-        if (k == 1) ccm0 = __ldg(com2 + ((int)d.x - 1));
+        // common-row pair at r0 (bilinear: x = r0 + 1; nearest: x = ir + 0.5)
+        const int rc = NEAR ? (int)d.x : (int)d.x - 1;
+        if ((k & 1) == 0) cc[k >> 1] = __ldg(com2 + rc);
+        if (k == 1) ccm0 = __ldg(com2 + rc);
       } else {
         fre[k] = fim[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         if constexpr (FULL) fre2[k] = fim2[k] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -927,17 +951,24 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
         const float2 lo = mir ? r1v : r0v, hi = mir ? r0v : r1v;
         return make_float2(fmaf(u, hi.x - lo.x, lo.x), fmaf(u, hi.y - lo.y, lo.y));
       };
-      const float2 b1 = bil(fre[k], fim[k]);
       float2 val;
-      if constexpr (FULL) {
+      if constexpr (NEAR) {
+        // the sample at (it, ir) plus the real common row at ir
+        const float2 v = make_float2(fre[k].x, fre[k].y);
+        val = mir ? cconj(v) : v;
+        val.x += c.x;
+      } else if constexpr (FULL) {
+        const float2 b1 = bil(fre[k], fim[k]);
         // direct: 0.5 (C(theta) + conj C(theta + pi)); mirror (conjugate of
         // the reflection): 0.5 (conj C(pi - theta) + C(2 pi - theta))
         const float2 b2 = bil(fre2[k], fim2[k]);
         val = make_float2(0.5f * (b1.x + b2.x), mir ? 0.5f * (b2.y - b1.y) : 0.5f * (b1.y - b2.y));
+        val.x += fmaf(r, c.y - c.x, c.x);
       } else {
+        const float2 b1 = bil(fre[k], fim[k]);
         val = mir ? cconj(b1) : b1;  // lower half plane: conjugate of the reflection
+        val.x += fmaf(r, c.y - c.x, c.x);
       }
-      val.x += fmaf(r, c.y - c.x, c.x);
       const int idx = mir ? (j == 0 ? mb0 : (L - t) - j * TPF) : t + j * TPF;
       if constexpr (MODF)  // exp(i pi b_signed / L) / exp(i pi t_owner / L), slot j or RPT-1-j
         val = mul_e32(val, slot_e(mir ? RPT - 1 - j : j));

@@ -111,12 +111,15 @@ struct Launch {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_PLAIN>, a, (int)smem_k2());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_TEX>, a, (int)smem_k2());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_TEXF>, a, (int)smem_k2());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(tb::k2_columns<L, CH, tb::K2_TEXN>, a, (int)smem_k2());
     return e;
   }
   template <bool CH>
   static void launch_k2(const DevPlan& dp, const Work& w, dim3 g2, cudaStream_t st, int kc, int spc, int B, int sf) {
-    const bool tex = dp.interp == 0 && w.polar_tex && dp.gridtab2;
-    if (tex && dp.full_turn)
+    const bool tex = w.polar_tex && dp.gridtab2;  // the plan built the table for its interp / turn
+    if (tex && dp.interp != 0)
+      tb::k2_columns<L, CH, tb::K2_TEXN><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
+    else if (tex && dp.full_turn)
       tb::k2_columns<L, CH, tb::K2_TEXF><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
     else if (tex)
       tb::k2_columns<L, CH, tb::K2_TEX><<<g2, K2::THREADS, smem_k2(), st>>>(dp, w, kc, spc, B, sf);
@@ -217,7 +220,7 @@ struct Launch {
     mark(2, 1);
     const bool half = L >= 64 && 2 * p->n == L;
     mark(3, 0);
-    const bool tex = dp.interp == 0 && w.polar_tex && dp.gridtab2;
+    const bool tex = w.polar_tex && dp.gridtab2;
     const int kc = k2_cols(p, tex);
     const int spc = k2_slices(B);
     const int ncg = (p->H + 1 + kc - 1) / kc, nsg = (B + spc - 1) / spc;

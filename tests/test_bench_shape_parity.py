@@ -198,3 +198,23 @@ def test_full_turn_texture_path_against_oracle_and_lattice_path(monkeypatch):
     lat = F.fbp_volume(vol, plan, full_turn=True, batch=8)
     d = (torch.linalg.norm(lat - out) / torch.linalg.norm(lat)).item()
     assert d < 2e-5, d
+
+
+def test_nearest_texture_path_against_oracle_and_lattice_path(monkeypatch):
+    """interp="nearest" on the point-sampled texture path K2_TEXN (rounded
+    indices decided in fp64 at plan time, the mirror node's own rounded row):
+    three launch groups against the oracle, and against the lattice_value
+    path (TB_NOTEX=1 -> K2_ANY)."""
+    F = _F()
+    N, S = 512, 20
+    plan = F.BstPlan(N, N, interp="nearest")
+    vol = _noisy_volume(S, N, seed=9)
+    out = F.fbp_volume(vol, plan, batch=8)
+    op = O.OraclePlan(N, N, interp="nearest")
+    for k in (0, 7, 8, 19):
+        ref = O.fbp(vol[k].cpu().numpy().astype(np.float64), op)
+        _assert_close(out[k].cpu().numpy(), ref)
+    monkeypatch.setenv("TB_NOTEX", "1")
+    lat = F.fbp_volume(vol, plan, batch=8)
+    d = (torch.linalg.norm(lat - out) / torch.linalg.norm(lat)).item()
+    assert d < 2e-6, d
