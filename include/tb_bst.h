@@ -16,6 +16,7 @@
  *   tb_normalize                      <- preprocess.normalize      preprocess.py:59-74
  *   tb_center_estimate / _apply       <- estimate/apply_center     preprocess.py:88-138
  *   tb_rings                          <- suppress_rings            preprocess.py:141-154
+ *   tb_pre_params / tb_fbp_pre        <- center + rings + fbp      pipeline.py:461-518 (stages fused into K1)
  *   tb_fbp_counts                     <- normalize + fbp stages    pipeline.py:447-459, 486-518
  *   tb_fbp_frames                     <- read (layout 0) + fbp     volio.py:159-180, pipeline.py:486-518
  *
@@ -44,7 +45,7 @@
 extern "C" {
 #endif
 
-#define TB_ABI_VERSION 2
+#define TB_ABI_VERSION 3
 
 typedef enum {
   TB_OK = 0,
@@ -179,6 +180,20 @@ int tb_center_apply(const tb_plan* plan, const float* sino, const double* beta_c
  * odd `window` >= 3.  scratch: device [B][n_t] doubles.  May not alias. */
 int tb_rings(const tb_plan* plan, const float* sino, float* out, int window, double* scratch,
              int n_slices, void* stream);
+
+/* Fused centre / ring stages.  tb_pre_params: per slice the apply_center
+ * shift (floor(beta), frac(beta)) as float pairs shift[n_slices][2], from
+ * beta_conf[n_slices][2] (tb_center_estimate output or caller-filled; NULL =
+ * beta 0), and with window > 0 (odd >= 3) the suppress_rings stripe profile
+ * stripe[n_slices][n_t] of the centred sinogram (mean_scratch: n_slices * n_t
+ * doubles).  tb_fbp_pre: tb_fbp whose radial kernel applies the shift and
+ * subtracts the stripes as it loads each row (preprocess.py:119-154), with
+ * stripe NULL for centring only; TB_ERR_UNSUPPORTED unless the plan fuses
+ * the ramp filter into K1 (ramp_samples == radial_samples). */
+int tb_pre_params(const tb_plan* plan, const float* sino, int n_slices, const double* beta_conf, int window,
+                  double* mean_scratch, float* shift, float* stripe, void* stream);
+int tb_fbp_pre(const tb_plan* plan, const float* sino, float* image, int n_slices, int batch, void* ws,
+               size_t ws_bytes, const float* shift, const float* stripe, void* stream);
 
 /* BST backprojection only (input already ramp-filtered; no 1/(2 pi)). */
 int tb_bst(const tb_plan* plan, const float* sino, float* image, int n_slices,

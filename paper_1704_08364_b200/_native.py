@@ -102,6 +102,8 @@ def _bind(lib):
         "tb_center_estimate": (I, [P, P, I, P, P, P]),
         "tb_center_apply": (I, [P, P, P, P, I, P]),
         "tb_rings": (I, [P, P, P, I, P, I, P]),
+        "tb_pre_params": (I, [P, P, I, P, I, P, P, P, P]),
+        "tb_fbp_pre": (I, [P, P, P, I, I, P, S, P, P, P]),
         "tb_copy_polar": (I, [P, P, I, P, P]),
         "tb_reset_status": (I, [P, P, P]),
         "tb_read_status": (I, [P, P, P]),

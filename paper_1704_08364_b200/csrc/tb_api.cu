@@ -115,6 +115,8 @@ Work work_for(const tb_plan* p, int B, void* ws, int lane = 0) {
   w.filtered = reinterpret_cast<float*>(base + l.filtered);
   w.status = reinterpret_cast<int*>(static_cast<char*>(ws) + l.status);
   w.normtab = nullptr;
+  w.pre_shift = nullptr;
+  w.pre_stripe = nullptr;
   w.norm_eps = 0.f;
   w.norm_c = make_float2(0.f, 0.f);
   w.in_slice = (long long)p->rows * p->n_t;  // slice-major input by default
@@ -278,7 +280,8 @@ struct NormFrames {
 
 int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, int batch, void* ws,
                  size_t ws_bytes, void* stream, bool ramp, float scale, double* stage_ms = nullptr,
-                 const NormFrames* norm = nullptr, bool frame_major = false) {
+                 const NormFrames* norm = nullptr, bool frame_major = false, const float2* pre_shift = nullptr,
+                 const float* pre_stripe = nullptr) {
   int rc = check_exec_args(p, sino, img, n_slices, batch, ws, ws_bytes);
   if (rc) return rc;
   if (!p->bst_ok)
@@ -305,7 +308,7 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
   const size_t out_stride = (size_t)p->n * p->n;
   const int ngroups = (n_slices + batch - 1) / batch;
   // the fused schedule (one stream, two workspace lanes) where it applies
-  if (!stage_ms && ramp && fuse_cfg() > 0 && lanes_cfg() >= 2 && ngroups >= 2) {
+  if (!stage_ms && ramp && !pre_shift && fuse_cfg() > 0 && lanes_cfg() >= 2 && ngroups >= 2) {
     Work lw[2];
     for (int l = 0; l < 2; ++l) {
       lw[l] = work_for(p, batch, ws, l);
@@ -356,6 +359,8 @@ int run_bst_like(const tb_plan* p, const float* sino, float* img, int n_slices, 
       w.norm_eps = (float)norm->eps;
       w.norm_c = norm_c;
     }
+    w.pre_shift = pre_shift ? pre_shift + s0 : nullptr;
+    w.pre_stripe = pre_stripe ? pre_stripe + (size_t)s0 * p->n_t : nullptr;
     cudaStream_t ls = lane ? aux[lane] : st;
     rc = bst_dispatch(p, sino + s0 * in_stride, img + s0 * out_stride, B, w, ramp, scale, ls,
                       stage_ms ? evs.data() + (size_t)g * 10 : nullptr);
@@ -974,12 +979,45 @@ int tb_rings(const tb_plan* p, const float* sino, float* out, int window, double
     const int B = std::min(65535, n_slices - s);
     dim3 grid((p->n_t + 255) / 256, B);
     const float* in = sino + (size_t)s * p->rows * p->n_t;
-    tb::k_col_mean<<<grid, 256, 0, st>>>(in, scratch, p->rows, p->n_t);
+    tb::k_col_mean<<<dim3((p->n_t + 31) / 32, B), dim3(32, 8), 0, st>>>(in, scratch, p->rows, p->n_t);
     tb::k_rings_apply<<<grid, 256, 0, st>>>(in, out + (size_t)s * p->rows * p->n_t, scratch, p->rows, p->n_t,
                                              window);
   }
   TB_CUDA(cudaGetLastError());
   return TB_OK;
+}
+
+int tb_pre_params(const tb_plan* p, const float* sino, int n_slices, const double* beta_conf, int window,
+                  double* mean_scratch, float* shift, float* stripe, void* stream) {
+  int rc = check_rows_call(p, sino, shift, n_slices);
+  if (rc) return rc;
+  if (window != 0 && (window < 3 || window % 2 == 0))
+    return fail(TB_ERR_INVALID, "window must be an odd integer >= 3, got " + std::to_string(window));
+  if (n_slices > 0 && window && (!mean_scratch || !stripe)) return fail(TB_ERR_INVALID, "null scratch / stripe pointer");
+  if (n_slices == 0) return TB_OK;
+  if ((rc = set_device(p))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int s = 0; s < n_slices; s += 65535) {
+    const int B = std::min(65535, n_slices - s);
+    if (window)
+      tb::k_col_mean<<<dim3((p->n_t + 31) / 32, B), dim3(32, 8), 0, st>>>(sino + (size_t)s * p->rows * p->n_t,
+                                                                          mean_scratch, p->rows, p->n_t);
+    tb::k_pre_params<<<B, 256, 0, st>>>(beta_conf ? beta_conf + 2 * (size_t)s : nullptr, mean_scratch, p->n_t, window,
+                                        reinterpret_cast<float2*>(shift) + s,
+                                        window ? stripe + (size_t)s * p->n_t : nullptr);
+  }
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_fbp_pre(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws,
+               size_t ws_bytes, const float* shift, const float* stripe, void* stream) {
+  if (!p) return fail(TB_ERR_INVALID, "null plan");
+  if (n_slices > 0 && !shift) return fail(TB_ERR_INVALID, "null shift pointer");
+  // the stages act on the raw rows, so K1 must run the ramp filter itself
+  if (p->npad != p->L) return fail(TB_ERR_UNSUPPORTED, "fused centre / rings need the ramp fused into K1 (npad == L)");
+  return run_bst_like(p, sino, image, n_slices, batch, ws, ws_bytes, stream, true, (float)(1.0 / (2.0 * kPi)),
+                      nullptr, nullptr, false, reinterpret_cast<const float2*>(shift), stripe);
 }
 
 int tb_fbp_ss(const tb_plan* p, const float* sino, float* image, int n_slices, int batch, void* ws,

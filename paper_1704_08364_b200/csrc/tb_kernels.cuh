@@ -81,6 +81,11 @@ struct Work {
   // texture view of this lane's polar region (pitch 2D, float2 texels,
   // width H, height B*(V+1)); 0 = use plain loads
   cudaTextureObject_t polar_tex;
+  // fused centre / ring stages (preprocess.py:119-154) on K1's load, or null:
+  // per slice (floor(beta), frac(beta)) of the detector shift and the stripe
+  // profile [B][n_t] subtracted after it (k_pre_params)
+  const float2* pre_shift;
+  const float* pre_stripe;
 };
 
 #ifndef TB_K1_SLOTS
@@ -150,7 +155,7 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
   const int H = L / 2;
   const float* slice = sino + (size_t)q * w.in_slice;
   // bulk copies need 16-byte aligned rows; otherwise read rows directly
-  const bool bulk = TB_K1_SLOTS > 0 && (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0) && (w.in_row & 3) == 0 &&
+  const bool bulk = TB_K1_SLOTS > 0 && !w.pre_shift && (p.n_t & 3) == 0 && ((reinterpret_cast<uintptr_t>(sino) & 15) == 0) && (w.in_row & 3) == 0 &&
                     (w.in_slice & 3) == 0;
   auto issue = [&](int pr, int slot) {
     // the slot was last read by generic-proxy loads (ordered before this
@@ -229,8 +234,20 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
         // n_t <= L/2 always (L >= pad_factor * n_t, pad_factor >= 2): the upper
         // half of every padded row is a compile-time zero (pruned first pass)
         if (i < RPT / 2 && active && idx < p.n_t) {
-          a = __ldg(y0 + idx);
-          if (has1) b = __ldg(y1 + idx);
+          if (w.pre_shift) {
+            // apply_center (linear interpolation at idx + beta, 0 outside the
+            // detector) then the ring stripe: preprocess.py:119-154
+            const float2 sh = __ldg(w.pre_shift + q);
+            const int j = idx + (int)sh.x;
+            const bool ok0 = j >= 0 && j <= p.n_t - 1, ok1 = j + 1 >= 0 && j + 1 <= p.n_t - 1;
+            const float w0 = 1.f - sh.y, w1 = sh.y;
+            const float st = w.pre_stripe ? __ldg(w.pre_stripe + (size_t)q * p.n_t + idx) : 0.f;
+            a = (ok0 ? w0 * __ldg(y0 + j) : 0.f) + (ok1 ? w1 * __ldg(y0 + j + 1) : 0.f) - st;
+            if (has1) b = (ok0 ? w0 * __ldg(y1 + j) : 0.f) + (ok1 ? w1 * __ldg(y1 + j + 1) : 0.f) - st;
+          } else {
+            a = __ldg(y0 + idx);
+            if (has1) b = __ldg(y1 + idx);
+          }
           if constexpr (NORM) {
             if (w.normtab) {
               const float2* nt = w.normtab + (size_t)j0 * p.n_t + idx;
@@ -1515,16 +1532,27 @@ __global__ void __launch_bounds__(256) k_center_apply(const float* __restrict__ 
       (float)((double)r[i0c] * (ok0 ? 1.0 - fr : 0.0) + (double)r[i1c] * (ok1 ? fr : 0.0));
 }
 
-// per-detector mean over angles (fp64), mean[q][i]
+// per-detector mean over angles (fp64), mean[q][i]: a (32, 8) block per 32
+// detector columns of one slice, 8 row groups summed in parallel (coalesced
+// 128-B row segments) and combined in shared memory.  Launch: grid
+// (ceil(n_t / 32), slices), block (32, 8).
 __global__ void __launch_bounds__(256) k_col_mean(const float* __restrict__ in, double* __restrict__ mean, int rows,
                                                   int n_t) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double part[8][33];
+  const int i = blockIdx.x * 32 + threadIdx.x;
   const int q = blockIdx.y;
-  if (i >= n_t) return;
-  const float* y = in + (size_t)q * rows * n_t + i;
   double s = 0.0;
-  for (int j = 0; j < rows; ++j) s += (double)y[(size_t)j * n_t];
-  mean[(size_t)q * n_t + i] = s / rows;
+  if (i < n_t) {
+    const float* y = in + (size_t)q * rows * n_t + i;
+    for (int j = threadIdx.y; j < rows; j += 8) s += (double)__ldg(y + (size_t)j * n_t);
+  }
+  part[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < n_t) {
+    double t = 0.0;
+    for (int g = 0; g < 8; ++g) t += part[g][threadIdx.x];
+    mean[(size_t)q * n_t + i] = t / rows;
+  }
 }
 
 // out = in - (mean - movavg_window(reflect-pad(mean)))  (preprocess.py:141-154)
@@ -1546,6 +1574,40 @@ __global__ void __launch_bounds__(256) k_rings_apply(const float* __restrict__ i
   const float* y = in + (size_t)q * rows * n_t + i;
   float* o = out + (size_t)q * rows * n_t + i;
   for (int j = 0; j < rows; ++j) o[(size_t)j * n_t] = (float)((double)y[(size_t)j * n_t] - stripe);
+}
+
+// Fused centre / ring parameters per slice (one CTA each): the shift
+// (floor(beta), frac(beta)) of apply_center and, with window > 0, the
+// stripe profile of suppress_rings computed from the column means of the
+// CENTRED data, which are the centred column means of the raw data (the
+// interpolation is the same linear map on every row): stripe = c - movavg(
+// reflect-pad(c)), c = apply_center(mean).  preprocess.py:119-154.
+__global__ void __launch_bounds__(256) k_pre_params(const double* __restrict__ beta_conf, const double* __restrict__ mean,
+                                                    int n_t, int window, float2* __restrict__ shift,
+                                                    float* __restrict__ stripe) {
+  const int q = blockIdx.x;
+  const double beta = beta_conf ? beta_conf[2 * q] : 0.0;
+  const double bf = floor(beta);
+  const double fr = beta - bf;
+  const int bi = (int)bf;
+  if (threadIdx.x == 0) shift[q] = make_float2((float)bi, (float)fr);
+  if (window <= 0) return;
+  const double* m = mean + (size_t)q * n_t;
+  auto centred = [&](int k) {
+    const int j = k + bi;
+    const bool ok0 = j >= 0 && j <= n_t - 1, ok1 = j + 1 >= 0 && j + 1 <= n_t - 1;
+    return (ok0 ? m[j] * (1.0 - fr) : 0.0) + (ok1 ? m[j + 1] * fr : 0.0);
+  };
+  const int h = window / 2;
+  for (int i = threadIdx.x; i < n_t; i += blockDim.x) {
+    double acc = 0.0;
+    for (int d = -h; d <= h; ++d) {
+      int k = i + d;
+      while (k < 0 || k > n_t - 1) k = k < 0 ? -k : 2 * (n_t - 1) - k;  // np.pad(mode="reflect")
+      acc += centred(k) * (1.0 / window);
+    }
+    stripe[(size_t)q * n_t + i] = (float)(centred(i) - acc);
+  }
 }
 
 // standalone normalize over n slices of [rows][n_t] counts

@@ -331,10 +331,37 @@ class NativePlan:
                                 int(window), ctypes.c_void_p(scratch.data_ptr()), int(n_slices), self._stream(stream))
         _native.check(rc, "tb_rings")
 
+    def pre_params(self, sino: torch.Tensor, n_slices: int, beta_conf: torch.Tensor | None, window: int,
+                   stream=None) -> tuple[torch.Tensor, torch.Tensor | None]:
+        """Fused centre / ring stage parameters (tb_pre_params): shift [S][2]
+        f32 (floor(beta), frac(beta)) and, with window > 0, the stripe
+        profile [S][n_t] f32 of the centred sinogram."""
+        dev = f"cuda:{self.device}"
+        shift = torch.empty((max(n_slices, 1), 2), dtype=torch.float32, device=dev)
+        stripe = torch.empty((max(n_slices, 1), self.n_t), dtype=torch.float32, device=dev) if window else None
+        scratch = torch.empty((max(n_slices, 1), self.n_t), dtype=torch.float64, device=dev) if window else None
+        rc = self._lib.tb_pre_params(self._h, ctypes.c_void_p(sino.data_ptr()), int(n_slices),
+                                     ctypes.c_void_p(beta_conf.data_ptr() if beta_conf is not None else None),
+                                     int(window), ctypes.c_void_p(scratch.data_ptr() if window else None),
+                                     ctypes.c_void_p(shift.data_ptr()),
+                                     ctypes.c_void_p(stripe.data_ptr() if window else None), self._stream(stream))
+        _native.check(rc, "tb_pre_params")
+        return shift, stripe
+
+    def run_pre(self, sino: torch.Tensor, image: torch.Tensor, n_slices: int, batch: int, workspace: torch.Tensor,
+                shift: torch.Tensor, stripe: torch.Tensor | None, stream=None) -> None:
+        """tb_fbp with the centre / ring stages applied on K1's load (tb_fbp_pre)."""
+        rc = self._lib.tb_fbp_pre(self._h, ctypes.c_void_p(sino.data_ptr()), ctypes.c_void_p(image.data_ptr()),
+                                  int(n_slices), int(batch), ctypes.c_void_p(workspace.data_ptr()),
+                                  ctypes.c_size_t(workspace.numel()), ctypes.c_void_p(shift.data_ptr()),
+                                  ctypes.c_void_p(stripe.data_ptr() if stripe is not None else None),
+                                  self._stream(stream))
+        _native.check(rc, "tb_fbp_pre")
+
     def polar(self, workspace: torch.Tensor, batch: int, stream=None) -> torch.Tensor:
         """K1 output of the last launch group (first lane) on this workspace:
         [batch][rows][L/2] complex64 (tb_copy_polar)."""
-        rows = self.n_angles + 1 if not self.full_turn else self.n_angles
+        rows = self.n_angles + 1  # + the angle-pi (half turn) / angle-2 pi (full turn) copy of row 0
         out = torch.empty((batch, rows, self.L // 2), dtype=torch.complex64, device=f"cuda:{self.device}")
         _native.check(self._lib.tb_copy_polar(self._h, ctypes.c_void_p(workspace.data_ptr()), int(batch),
                                               ctypes.c_void_p(out.data_ptr()), self._stream(stream)), "tb_copy_polar")
@@ -540,9 +567,12 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
 
     ``center`` ("auto": per-slice estimate_center; a float: that beta for
     every slice) and ``rings`` (odd window) run the reference pipeline's
-    center and rings stages (pipeline.py:461-484) on the device before the
-    reconstruction (device input); an implausible or undetermined centre
-    raises CenteringError like the reference.
+    center and rings stages (pipeline.py:461-484) on the device (device
+    input): for kernel "bst" without frames they are fused into the radial
+    kernel's row load (tb_fbp_pre: per-slice shift and stripe profile, no
+    extra sinogram passes), otherwise separate passes before the
+    reconstruction; an implausible or undetermined centre raises
+    CenteringError like the reference.
 
     ``scale`` (kernel "none" only) multiplies the backprojection inside the
     last kernel's epilogue (the pipeline's bst_backproject x FBP_SCALE).
@@ -572,10 +602,22 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
         batch = default_batch(plan, full_turn)
     if (center is not None or rings is not None) and not sino.is_cuda:
         raise ValueError("center / rings stages run on device-resident volumes")
+    pre = None
     if sino.is_cuda and S and (center is not None or rings is not None):
-        from .preprocess import preprocess_volume
-        sino = preprocess_volume(sino, plan, full_turn, frames=frames, eps=eps, center=center, rings=rings)
-        frames = None  # normalised by the preprocessing pass
+        from .preprocess import center_beta, preprocess_volume
+        one_dev = devices is None or [_device_index(d) for d in devices] == [sino.device.index]
+        if (frames is None and op == "fbp" and one_dev and plan.radial_samples == 2 * _next_pow2(n_t)):
+            # centre and ring stages fused into K1's row load (tb_fbp_pre):
+            # per-slice shift and stripe profile, no extra sinogram passes
+            if rings is not None and (rings < 3 or rings % 2 == 0):
+                raise ValueError(f"window must be an odd integer >= 3, got {rings}")
+            dev = sino.device.index
+            with torch.cuda.device(dev):
+                bc = center_beta(sino, S, A, n_t, full_turn, center) if center is not None else None
+                pre = native_plan(plan, fplan, full_turn, dev).pre_params(sino, S, bc, rings or 0)
+        else:
+            sino = preprocess_volume(sino, plan, full_turn, frames=frames, eps=eps, center=center, rings=rings)
+            frames = None  # normalised by the preprocessing pass
     if sino.is_cuda and devices is not None and frames is None and S:
         devs = [_device_index(d) for d in devices]
         if devs != [sino.device.index]:
@@ -596,6 +638,8 @@ def fbp_volume(sino, plan: BstPlan | None = None, fplan: FilterPlan = FilterPlan
                     line = torch.empty_like(sino)
                     nat.normalize(sino, flat, dark, eps, line, S)
                     nat.run(op, line, out, S, min(batch, S), ws, scale=scale)
+            elif S and pre is not None:
+                nat.run_pre(sino, out, S, min(batch, S), ws, pre[0], pre[1])
             elif S:
                 nat.run(op, sino, out, S, min(batch, S), ws, scale=scale)
             if check:

@@ -136,6 +136,29 @@ def suppress_rings(y, window: int = 9, device=None):
     return Sinogram(y.detector, y.angles, out[0].cpu().numpy().astype(np.float64))
 
 
+def center_beta(sino: torch.Tensor, S: int, A: int, n_t: int, full_turn: bool, center) -> torch.Tensor:
+    """Per-slice (beta, confidence) [S][2] float64 device tensor for the
+    centre stage: "auto" estimates every slice (estimate_center,
+    preprocess.py:88-116; CenteringError as the reference raises it), a
+    number is that beta for every slice (apply_center's range check)."""
+    from . import fourier_bp as F
+    if isinstance(center, str):
+        if center != "auto":
+            raise ValueError(f"unknown center mode {center!r}")
+        nat = F.aux_plan(n_t, A, full_turn, device=sino.device.index)
+        bc, st = nat.center_estimate(sino, S)
+        bad = torch.nonzero(st).flatten()
+        if bad.numel():
+            k = int(bad[0].item())
+            _raise_centering(int(st[k].item()), float(bc[k, 0].item()))
+        return bc
+    if abs(float(center)) > n_t:
+        raise ValueError(f"shift of {center} bins exceeds the detector extent")
+    bc = torch.zeros((S, 2), dtype=torch.float64, device=sino.device)
+    bc[:, 0] = float(center)
+    return bc
+
+
 def preprocess_volume(sino: torch.Tensor, plan, full_turn: bool = False, frames=None, eps: float = 1e-6,
                       center=None, rings: int | None = None) -> torch.Tensor:
     """normalize -> center -> rings over a device-resident volume [S][A][n_t]
@@ -155,19 +178,7 @@ def preprocess_volume(sino: torch.Tensor, plan, full_turn: bool = False, frames=
             nat.normalize(x, flat, dark, eps, y, S)
             x = y
         if center is not None:
-            if isinstance(center, str):
-                if center != "auto":
-                    raise ValueError(f"unknown center mode {center!r}")
-                bc, st = nat.center_estimate(x, S)
-                bad = torch.nonzero(st).flatten()
-                if bad.numel():
-                    k = int(bad[0].item())
-                    _raise_centering(int(st[k].item()), float(bc[k, 0].item()))
-            else:
-                if abs(float(center)) > n_t:
-                    raise ValueError(f"shift of {center} bins exceeds the detector extent")
-                bc = torch.zeros((S, 2), dtype=torch.float64, device=sino.device)
-                bc[:, 0] = float(center)
+            bc = center_beta(x, S, A, n_t, full_turn, center)
             y = torch.empty_like(x)
             nat.center_apply(x, bc, y, S)
             x = y

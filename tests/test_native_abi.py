@@ -14,7 +14,7 @@ def test_library_loads_and_exports_every_header_symbol():
     assert len(names) >= 14
     for name in names:
         assert hasattr(lib, name), name
-    assert lib.tb_abi_version() == 2
+    assert lib.tb_abi_version() == 3
 
 
 def _desc(**kw):

@@ -103,3 +103,44 @@ def test_gpu_constant_sinogram_raises_centering_error():
     vol = torch.full((2, 16, 32), 3.0, device="cuda")
     with pytest.raises(CenteringError, match="constant sinogram"):
         F.fbp_volume(vol, F.BstPlan(32, 16), center="auto")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("center,rings", [("auto", 9), (3.25, None), (None, 5), (-7.5, 11)])
+def test_gpu_fused_center_rings_equal_separate_passes(center, rings):
+    """fbp_volume with the centre / ring stages fused into K1's row load
+    (tb_fbp_pre) against the separate device passes (preprocess_volume, then
+    fbp) on a 6-slice 512^2 volume over three launch groups."""
+    torch = _cuda()
+    from paper_1704_08364_b200 import fourier_bp as F
+    from paper_1704_08364_b200 import phantom
+    from paper_1704_08364_b200.preprocess import preprocess_volume
+    N = 512
+    plan = F.BstPlan(N, N)
+    vol = phantom.ellipsoid_volume(6, N, N, device="cuda")
+    g = torch.Generator("cuda").manual_seed(2)
+    vol += 0.02 * torch.randn(vol.shape, device="cuda", generator=g)
+    vol += 0.05 * torch.rand((1, 1, N), device="cuda", generator=g)  # detector stripes
+    vol = torch.roll(vol, 3, dims=2)
+    fused = F.fbp_volume(vol, plan, center=center, rings=rings, batch=2)
+    sep = F.fbp_volume(preprocess_volume(vol, plan, center=center, rings=rings), plan, batch=2)
+    for k in range(6):
+        d = (torch.linalg.norm(fused[k] - sep[k]) / torch.linalg.norm(sep[k])).item()
+        assert d < 1e-5, (k, d)
+
+
+@pytest.mark.gpu
+def test_gpu_fused_stages_fall_back_when_the_ramp_is_not_fused():
+    """A plan whose ramp is a separate pass (pad_factor 4: npad != L) takes
+    the separate preprocessing passes: same result as doing them by hand."""
+    torch = _cuda()
+    from paper_1704_08364_b200 import fourier_bp as F
+    from paper_1704_08364_b200 import phantom
+    from paper_1704_08364_b200.preprocess import preprocess_volume
+    plan = F.BstPlan(128, 128, pad_factor=4)
+    vol = phantom.ellipsoid_volume(2, 128, 128, device="cuda")
+    g = torch.Generator("cuda").manual_seed(4)
+    vol += 0.05 * torch.rand(vol.shape, device="cuda", generator=g)
+    a = F.fbp_volume(vol, plan, center=2.5, rings=5)
+    b = F.fbp_volume(preprocess_volume(vol, plan, center=2.5, rings=5), plan)
+    assert torch.equal(a, b)
