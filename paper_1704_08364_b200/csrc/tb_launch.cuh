@@ -147,6 +147,7 @@ struct Launch {
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
     TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1b));
     TB_CUDA(set_k2_smem<false>());
     TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
@@ -172,6 +173,7 @@ struct Launch {
         const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
         TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false>, co, c1));
         TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, true>, co, c1));
+        TB_CUDA(cudaFuncSetAttribute(tb::k1_radial<L, true, false, true>, co, c1));
         TB_CUDA(cudaFuncSetAttribute(tb::k2_columns<L, (L >= 64), tb::K2_TEX>, co, c2));
         TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, (L >= 64)>, co, c3));
       }
@@ -210,6 +212,8 @@ struct Launch {
     mark(1, 0);
     if (fused && wk.norm_eps > 0.f)  // transmission counts: normalisation fused into the load
       tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
+    else if (fused && wk.pre_shift)  // centre / ring stages fused into the load (tb_fbp_pre)
+      tb::k1_radial<L, true, false, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else if (fused)
       tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else
