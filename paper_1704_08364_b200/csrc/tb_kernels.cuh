@@ -745,8 +745,12 @@ __device__ __forceinline__ GridNode decode_node(const DevPlan& p, uint2 e, int a
 // K2 -> K3 intermediate: [B][ceil(n/4)][H+1][4] complex (4-row tiles = one
 // 32-byte sector per (tile, column)), so K2's column stores and K3's row-pair
 // loads both move whole sectors.
+#ifndef TB_COL_TILE
+#define TB_COL_TILE 4
+#endif
+constexpr int kColTile = TB_COL_TILE;  // rows per (tile, column) group of the K2 -> K3 intermediate
 __device__ __forceinline__ size_t col_index(int H, int m2, int a) {
-  return ((size_t)(m2 >> 2) * (H + 1) + a) * 4 + (m2 & 3);
+  return ((size_t)(m2 / kColTile) * (H + 1) + a) * kColTile + (m2 % kColTile);
 }
 
 // ---------------------------------------------------------------------------
@@ -1159,12 +1163,12 @@ __device__ __forceinline__ void k2_column(const DevPlan& p, const Work& w, int a
       // i >= 3 RPT/4 (m2 = t + (i - 3 RPT/4) TPF); m2 = t + c_i with c_i a
       // multiple of 4, so col_index is one per-thread base plus a
       // compile-time tile offset (the other slots are DCE'd)
-      float2* ob = out + (((size_t)(t >> 2) * (H + 1) + a) * 4 + (t & 3));
+      float2* ob = out + (((size_t)(t / kColTile) * (H + 1) + a) * kColTile + (t % kColTile));
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         if (i < RPT / 4 || i >= 3 * RPT / 4) {
           const int c = i < RPT / 4 ? i * TPF + L / 4 : (i - 3 * RPT / 4) * TPF;
-          ob[(size_t)(c / 4) * (H + 1) * 4] = v[i];
+          ob[(size_t)(c / kColTile) * (H + 1) * kColTile] = v[i];
         }
       }
     } else {
@@ -1266,7 +1270,7 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
   // blocks are exactly TPF threads once TPF >= 32: compile-time true there
   const bool active = TPF >= 32 || t < TPF;
   const int n = p.n;
-  const float2* G = w.columns + (size_t)q * p.col_slice + (size_t)tile * (H + 1) * 4;
+  const float2* Gs = w.columns + (size_t)q * p.col_slice;
   const float cm = __ldcg(w.coefmean + q);  // written by another CTA (K1b)
   const float inv_n = 2.f / (float)n;
   const float A = p.img_scale * out_scale;       // amplitude / L^2 / (2 pi)
@@ -1279,6 +1283,8 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
     // n = L/2 (CROP_HALF) is a multiple of 4: every tile holds 4 rows
     if (!CROP_HALF && m2a >= n) break;  // uniform across the CTA
     const bool hasb = CROP_HALF || m2b < n;
+    // the pair's two rows: 16 B per column at stride kColTile complex
+    const float2* G = Gs + (size_t)(m2a / kColTile) * (H + 1) * kColTile + (m2a % kColTile);
     float2 v[RPT];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -1286,7 +1292,7 @@ __device__ __forceinline__ void k3_tile(const DevPlan& p, const Work& w, float* 
       if (active) {
         // a = t + i TPF; bins a > H are the conjugates of L - a (i >= RPT/2)
         const int ar = (i < RPT / 2) ? t + i * TPF : L - (t + i * TPF);
-        const float4 g = __ldg(reinterpret_cast<const float4*>(G + (size_t)ar * 4 + 2 * pair));
+        const float4 g = __ldg(reinterpret_cast<const float4*>(G + (size_t)ar * kColTile));
         float2 ga = make_float2(g.x, g.y);
         float2 gb = hasb ? make_float2(g.z, g.w) : make_float2(0.f, 0.f);
         if (i >= RPT / 2) { ga.y = -ga.y; gb.y = -gb.y; }
