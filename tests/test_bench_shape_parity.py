@@ -218,3 +218,29 @@ def test_nearest_texture_path_against_oracle_and_lattice_path(monkeypatch):
     lat = F.fbp_volume(vol, plan, batch=8)
     d = (torch.linalg.norm(lat - out) / torch.linalg.norm(lat)).item()
     assert d < 2e-6, d
+
+
+@pytest.mark.parametrize("n_t,V,full,interp,out_n,pad", [
+    (128, 96, True, "bilinear", 100, 2),     # K2_TEXF without the half crop (per-node modulation)
+    (65, 33, True, "bilinear", 63, 2),       # odd sizes, full turn
+    (128, 96, False, "nearest", 100, 2),     # K2_TEXN without the half crop
+    (65, 33, False, "nearest", 63, 2),       # odd sizes, nearest
+    (64, 48, True, "bilinear", None, 4),     # full turn, separate ramp pass (npad != L)
+    (64, 48, False, "nearest", None, 4),     # nearest, separate ramp pass
+])
+def test_texture_paths_edge_shapes_against_oracle(n_t, V, full, interp, out_n, pad):
+    """The round-2 texture paths on shapes off the benchmark's: no n = L/2
+    crop (modulation per node instead of fft_mod), odd sizes, pad_factor 4,
+    three slices in launch groups of 2."""
+    F = _F()
+    plan = F.BstPlan(n_t, V, interp=interp, output_n=out_n, pad_factor=pad)
+    A = 2 * V if full else V
+    g = torch.Generator("cuda").manual_seed(n_t + V)
+    ell = O.ellipse_sinogram(O.SHEPP_LOGAN, n_t, A, full_turn=full)
+    vol = torch.from_numpy(ell.astype(np.float32)).cuda().expand(3, -1, -1).contiguous()
+    vol += 0.05 * torch.randn(vol.shape, device="cuda", generator=g)
+    out = F.fbp_volume(vol, plan, full_turn=full, batch=2)
+    op = O.OraclePlan(n_t, V, interp=interp, output_n=out_n, pad_factor=pad)
+    for k in range(3):
+        ref = O.fbp(vol[k].cpu().numpy().astype(np.float64), op, full_turn=full)
+        _assert_close(out[k].cpu().numpy(), ref)
