@@ -169,14 +169,15 @@ cudaTextureObject_t polar_texture(const tb_plan* p, const void* ptr, int rows) {
 cudaTextureObject_t image_texture(const tb_plan* p, const void* ptr, int rows) {
   if (rows > 65000 || p->n > 65000) return 0;
   if (const char* e = std::getenv("TB_NOTEX")) if (std::atoi(e) == 1) return 0;
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, p->device) != cudaSuccess) {
+  int talign = 0, palign = 0;  // cudaDeviceGetAttribute: cheap, unlike cudaGetDeviceProperties
+  if (cudaDeviceGetAttribute(&talign, cudaDevAttrTextureAlignment, p->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&palign, cudaDevAttrTexturePitchAlignment, p->device) != cudaSuccess || talign <= 0 ||
+      palign <= 0) {
     cudaGetLastError();
     return 0;
   }
   const size_t pitch = (size_t)p->n * sizeof(float);
-  if ((reinterpret_cast<uintptr_t>(ptr) % prop.textureAlignment) != 0 || pitch % prop.texturePitchAlignment != 0)
-    return 0;
+  if ((reinterpret_cast<uintptr_t>(ptr) % (uintptr_t)talign) != 0 || pitch % (size_t)palign != 0) return 0;
   std::lock_guard<std::mutex> lk(p->tex_mu);
   for (const auto& t : p->itexs)
     if (t.ptr == ptr && t.rows == rows) return t.obj;
