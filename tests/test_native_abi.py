@@ -63,3 +63,41 @@ def test_null_arguments_do_not_crash():
     assert lib.tb_plan_create(None, 0, None) == _native.TB_ERR_INVALID
     assert lib.tb_plan_destroy(None) == _native.TB_OK
     assert lib.tb_fbp(None, None, None, 1, 1, None, 0, None) == _native.TB_ERR_INVALID
+    assert lib.tb_fbp_pre(None, None, None, 1, 1, None, 0, None, None, None) == _native.TB_ERR_INVALID
+    assert lib.tb_pre_params(None, None, 1, None, 9, None, None, None, None) == _native.TB_ERR_INVALID
+
+
+@pytest.mark.gpu
+def test_fused_stage_entry_points_validate_like_the_reference():
+    """tb_pre_params / tb_fbp_pre error paths on a real plan: ring window
+    (suppress_rings' message), missing shift / stripe buffers, and a plan
+    whose ramp is a separate pass (npad != L) -> TB_ERR_UNSUPPORTED."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    lib = _native.lib()
+    h = ctypes.c_void_p()
+    assert lib.tb_plan_create(ctypes.byref(_desc(n_t=64, n_theta=32)), 0, ctypes.byref(h)) == _native.TB_OK
+    h4 = ctypes.c_void_p()
+    assert lib.tb_plan_create(ctypes.byref(_desc(n_t=64, n_theta=32, pad_factor=4)), 0,
+                              ctypes.byref(h4)) == _native.TB_OK
+    try:
+        sino = torch.zeros((2, 32, 64), device="cuda")
+        shift = torch.zeros((2, 2), device="cuda")
+        p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        assert lib.tb_pre_params(h, p(sino), 2, None, 4, None, p(shift), None, None) == _native.TB_ERR_INVALID
+        assert b"window must be an odd integer >= 3, got 4" in lib.tb_last_error()
+        assert lib.tb_pre_params(h, p(sino), 2, None, 9, None, p(shift), None, None) == _native.TB_ERR_INVALID
+        assert lib.tb_pre_params(h, p(sino), 2, None, 0, None, p(shift), None, None) == _native.TB_OK
+        img = torch.empty((2, 64, 64), device="cuda")
+        ws_bytes = ctypes.c_size_t()
+        assert lib.tb_workspace_bytes(h4, 2, ctypes.byref(ws_bytes)) == _native.TB_OK
+        ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device="cuda")
+        rc = lib.tb_fbp_pre(h4, p(sino), p(img), 2, 2, p(ws), ws_bytes, p(shift), None, None)
+        assert rc == _native.TB_ERR_UNSUPPORTED
+        rc = lib.tb_fbp_pre(h, p(sino), p(img), 2, 2, p(ws), ws_bytes, None, None, None)
+        assert rc == _native.TB_ERR_INVALID
+        torch.cuda.synchronize()
+    finally:
+        lib.tb_plan_destroy(h)
+        lib.tb_plan_destroy(h4)
