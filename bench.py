@@ -58,6 +58,8 @@ def _args():
     ap.add_argument("--no-ss", action="store_true", help="skip the slant-stack comparator sample")
     ap.add_argument("--no-counts", action="store_true", help="skip the fused-normalisation counts step")
     ap.add_argument("--ss-slices", type=int, default=8)
+    ap.add_argument("--ref-budget-s", type=float, default=240.0,
+                    help="--impl reference: wall-clock bound of its warm-up + timed steps (0 = run all)")
     return ap.parse_args()
 
 
@@ -105,20 +107,38 @@ def _cpu_sample(n, slices, threads):
     return dt, slices * n * n / dt
 
 
-def _cpu_reference(n, steps, warmup, threads):
+def _cpu_reference(n, steps, warmup, threads, budget_s=None):
     """The reference's own CPU path on this host: the unmodified tomoblocks
     pipeline (oracle/_ref, oracle/ref_bench.py) when installed, else the
-    oracle port.  Returns (voxels/s median, kind, sample, detail)."""
+    oracle port.  Returns (voxels/s median, kind, sample, detail).
+
+    ``budget_s`` bounds the wall clock of the warm-up plus timed steps (each
+    step is a (K_a, K_b) pair of pipeline runs, ~20 s at 2048 on 16 threads):
+    steps stop once the next one would overrun it (the first requested
+    warm-up step and one timed step always run); ``detail`` records how many
+    ran."""
     from oracle import ref_bench
     if ref_bench.available():
         rb = ref_bench.RefBench(n, threads)
+        t0 = time.perf_counter()
+        done_w, runs = 0, []
         try:
             for _ in range(warmup):
+                t1 = time.perf_counter()
                 rb.step(n)
-            runs = [rb.step(n) for _ in range(max(1, steps))]
+                done_w += 1
+                if budget_s and (time.perf_counter() - t0) + (time.perf_counter() - t1) * (max(1, steps) + 1) > budget_s:
+                    break  # keep the budget for the timed steps
+            for _ in range(max(1, steps)):
+                t1 = time.perf_counter()
+                runs.append(rb.step(n))
+                if budget_s and (time.perf_counter() - t0) + (time.perf_counter() - t1) > budget_s:
+                    break
         finally:
             rb.close()
         value = statistics.median(r["voxels_per_s"] for r in runs)
+        for r in runs:
+            r["warmup_steps_run"] = done_w
         return value, "reference", rb.describe(n), runs
     slices = max(threads, 4)
     for _ in range(warmup):
@@ -135,10 +155,12 @@ def run_reference(args):
     from oracle import ref_bench
     n = args.size
     threads = os.cpu_count() or 1
-    value, kind, sample, runs = _cpu_reference(n, args.steps, args.warmup, threads)
+    value, kind, sample, runs = _cpu_reference(n, args.steps, args.warmup, threads, args.ref_budget_s)
+    ran = len(runs) if runs else args.steps
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup,
+        "steps": ran, "warmup": runs[0]["warmup_steps_run"] if runs else args.warmup,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": 1e3 * (n ** 3) / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic ellipsoid phantom)",
         "config": _workload(n),
