@@ -798,14 +798,20 @@ struct K2Shape {
 #endif
   static constexpr int G = TPF >= TB_K2_THREADS ? 1 : TB_K2_THREADS / TPF;
   static constexpr int THREADS = G * TPF;
-// CTAs per SM asked of ptxas for <= 256-thread K2 CTAs: 4 (64 registers).
-// ptxas spills ~200 B per thread in the FFT phase, yet K2 drops 101.5 ->
-// 95.3 ms at 2048^3 (11.29 -> 11.15 at 1024^3, 1.46 -> 1.42 at 512^3): a
-// fourth resident column hides more gather latency than the spills cost
+// CTAs per SM asked of ptxas for <= 256-thread K2 CTAs: 4 (64 registers),
+// 5 at L = 4096 (48 registers).  Round 1: a fourth resident column hid more
+// gather latency than its spills cost (K2 101.5 -> 95.3 ms at 2048^3); with
+// the leaner pair gather a fifth pays at 2048^3 only (below)
 #ifndef TB_K2_MINB
 #define TB_K2_MINB 4
 #endif
-#define TB_K2_MINB_L(L) TB_K2_MINB
+// L = 4096 (2048^3): 5 CTAs per SM (48 registers, no spills with the pair
+// gather): step 160.1-160.4 -> 159.1-159.4 ms; at 1024^3 / 512^3 the fifth
+// CTA costs (19.79 -> 20.21, 2.52 -> 2.56 ms), so 4 there
+#ifndef TB_K2_MINB_4096
+#define TB_K2_MINB_4096 5
+#endif
+#define TB_K2_MINB_L(L) ((L) == 4096 ? TB_K2_MINB_4096 : TB_K2_MINB)
 #ifndef TB_K2_NAMED
 #define TB_K2_NAMED 1
 #endif
@@ -1225,7 +1231,12 @@ __device__ __forceinline__ void k2_block(const DevPlan& p, const Work& w, int cg
 }
 
 template <int L, bool CROP_HALF, int PATH>
-__global__ void __launch_bounds__(K2Shape<L>::THREADS, K2Shape<L>::MINB)
+// the fifth CTA per SM at L = 4096 only for the lean TLD4 paths (half-turn
+// bilinear / nearest); the full-turn and plain paths keep 4 (they spill at 48
+// registers: full turn 0.128 -> 0.133 ms per 2048^2 slice)
+__global__ void __launch_bounds__(K2Shape<L>::THREADS,
+                                  (PATH == K2_TEX || PATH == K2_TEXN) ? K2Shape<L>::MINB
+                                                                      : (K2Shape<L>::MINB > 4 ? 4 : K2Shape<L>::MINB))
     k2_columns(DevPlan p, Work w, int cols_per_cta, int slices_per_cta, int n_slices, int slice_fast) {
   extern __shared__ float2 smem[];
   // CTA = a run of columns x a run of slices; slice_fast puts the slice runs

@@ -83,7 +83,7 @@ struct Launch {
     // resident CTAs cover a few columns of every slice of the launch group,
     // so each 16 B-per-node table row is read from DRAM once per group)
     if (tex) return K2::G;
-    const int resident = K2::MINB;  // CTAs per SM
+    const int resident = std::min(K2::MINB, 4);  // CTAs per SM of the plain / general paths
     int steps = ((p->H + 1 + K2::G - 1) / K2::G + 148 * resident - 1) / (148 * resident);
     // L = 4096: the resident CTAs should cover a little less than one slice,
     // so the slice's polar spectrum and the gridding table stay in L2
