@@ -59,18 +59,24 @@ def _images(vol: torch.Tensor, n: int) -> list[ImageGrid]:
 
 
 def make_fbp_stage(plan: BstPlan, fplan: FilterPlan = FilterPlan(), kernel: str = "bst", workers: int = 1,
-                   queue_capacity: int = 4, device=None, frames=None, eps: float = 1e-6) -> StageSpec:
+                   queue_capacity: int = 4, device=None, frames=None, eps: float = 1e-6, center=None,
+                   rings: int | None = None) -> StageSpec:
     """Fused filter + backproject stage: Sinogram block -> ImageGrid block x 1/(2 pi)
     (pipeline.py:489-518 with cfg.kernel).  With ``frames`` (a
     preprocess.FlatDarkFrames) the blocks hold raw counts and the reference's
-    normalize stage (pipeline.py:447-459) runs fused into the same launch."""
+    normalize stage (pipeline.py:447-459) runs fused into the same launch.
+    ``center`` ("auto": estimate_center per slice; a number: cfg.center_beta)
+    and ``rings`` (cfg.ring_window) take over the center and rings stages
+    (pipeline.py:461-484) as well: for kernel "bst" without frames they are
+    applied on the radial kernel's row load."""
     if kernel not in ("ss", "bst"):
         raise ValueError(f"unknown kernel {kernel!r}")
     dev = _device_index(device)
 
     def process(block: VolumeBlock) -> VolumeBlock:
         vol, full = _stack(block, dev)
-        out = fbp_volume(vol, plan, fplan, kernel=kernel, full_turn=full, frames=frames, eps=eps)
+        out = fbp_volume(vol, plan, fplan, kernel=kernel, full_turn=full, frames=frames, eps=eps, center=center,
+                         rings=rings)
         return VolumeBlock(block.first_slice, _images(out, plan.output_n), StageKind.BACKPROJECT)
 
     return StageSpec("backproject", workers, queue_capacity, process, 2.0)

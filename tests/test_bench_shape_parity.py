@@ -244,3 +244,22 @@ def test_texture_paths_edge_shapes_against_oracle(n_t, V, full, interp, out_n, p
     for k in range(3):
         ref = O.fbp(vol[k].cpu().numpy().astype(np.float64), op, full_turn=full)
         _assert_close(out[k].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("center", ["auto", 2.5])
+def test_fbp_stage_with_center_and_rings_against_oracle(center):
+    """make_fbp_stage taking over the reference pipeline's center and rings
+    stages too (pipeline.py:461-518): the oracle runs estimate_center /
+    apply_center, suppress_rings, then fbp per slice."""
+    from paper_1704_08364_b200 import pipeline as P
+    F = _F()
+    vol = _noisy_volume(4, 128, seed=21)
+    vol = torch.roll(vol, 2, dims=2).contiguous()
+    blk, host = _block(vol, first=7)
+    spec = P.make_fbp_stage(F.BstPlan(128, 128), center=center, rings=9)
+    out = spec.process(blk)
+    op = O.OraclePlan(128, 128)
+    for i, img in enumerate(out.slices):
+        beta = O.estimate_center(host[i])[0] if center == "auto" else center
+        pre = O.suppress_rings(O.apply_center(host[i], beta), 9)
+        _assert_close(img.data, O.fbp(pre, op))
