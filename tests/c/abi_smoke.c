@@ -11,6 +11,8 @@
 
 #include <cuda_runtime_api.h>
 
+#include <string.h>
+
 #include "tb_bst.h"
 
 #define CHECK(x)                                                             \
@@ -64,6 +66,35 @@ int main(void) {
   if (!(worst <= 1e-4 * M_PI * c)) {
     fprintf(stderr, "constant-sinogram identity: max abs error %.3e\n", worst);
     return 1;
+  }
+  /* fused centre / ring stages (tb_pre_params + tb_fbp_pre): beta 0 and the
+   * stripes of a constant sinogram (0) leave tb_fbp's result bitwise intact */
+  {
+    float *shift = NULL, *stripe = NULL, *img2 = NULL;
+    double* scratch = NULL;
+    if (cudaMalloc((void**)&shift, (size_t)B * 2 * sizeof(float)) ||
+        cudaMalloc((void**)&stripe, (size_t)B * n * sizeof(float)) ||
+        cudaMalloc((void**)&scratch, (size_t)B * n * sizeof(double)) ||
+        cudaMalloc((void**)&img2, cnt * sizeof(float))) {
+      fprintf(stderr, "cudaMalloc failed\n");
+      return 1;
+    }
+    CHECK(tb_pre_params(plan, sino, B, NULL, 9, scratch, shift, stripe, NULL));
+    CHECK(tb_fbp(plan, sino, img, B, B, ws, ws_bytes, NULL));
+    CHECK(tb_fbp_pre(plan, sino, img2, B, B, ws, ws_bytes, shift, stripe, NULL));
+    CHECK(tb_read_status(plan, ws, NULL));
+    float* h2 = (float*)malloc(cnt * sizeof(float));
+    cudaMemcpy(host, img, cnt * sizeof(float), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h2, img2, cnt * sizeof(float), cudaMemcpyDeviceToHost);
+    if (memcmp(host, h2, cnt * sizeof(float)) != 0) {
+      fprintf(stderr, "tb_fbp_pre with zero shift / stripes differs from tb_fbp\n");
+      return 1;
+    }
+    free(h2);
+    cudaFree(shift);
+    cudaFree(stripe);
+    cudaFree(scratch);
+    cudaFree(img2);
   }
   tb_plan_desc bad = d;
   bad.n_t = 1;
