@@ -48,7 +48,13 @@ struct Trig16 {
                                   -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f};
 };
 
-// v * W_R^E with compile-time R | 16 and E (forward sign unless INV)
+// cos/sin(2 pi k / 64) (64-point transforms, 64 points per thread)
+struct Trig64 {
+  static constexpr float c[64] = {1.0f, 0.99518472667219693f, 0.98078528040323043f, 0.95694033573220882f, 0.92387953251128674f, 0.88192126434835505f, 0.83146961230254524f, 0.77301045336273699f, 0.70710678118654757f, 0.63439328416364549f, 0.55557023301960229f, 0.47139673682599781f, 0.38268343236508984f, 0.29028467725446233f, 0.19509032201612833f, 0.09801714032956077f, 0.0f, -0.098017140329560645f, -0.19509032201612819f, -0.29028467725446216f, -0.38268343236508973f, -0.4713967368259977f, -0.55557023301960196f, -0.63439328416364538f, -0.70710678118654746f, -0.77301045336273699f, -0.83146961230254535f, -0.88192126434835494f, -0.92387953251128674f, -0.95694033573220882f, -0.98078528040323043f, -0.99518472667219682f, -1.0f, -0.99518472667219693f, -0.98078528040323043f, -0.95694033573220894f, -0.92387953251128685f, -0.88192126434835505f, -0.83146961230254546f, -0.7730104533627371f, -0.70710678118654768f, -0.63439328416364593f, -0.55557023301960218f, -0.47139673682599786f, -0.38268343236509034f, -0.29028467725446244f, -0.19509032201612866f, -0.098017140329560451f, 0.0f, 0.09801714032956009f, 0.1950903220161283f, 0.29028467725446205f, 0.38268343236509f, 0.47139673682599759f, 0.55557023301960184f, 0.6343932841636456f, 0.70710678118654735f, 0.77301045336273666f, 0.83146961230254524f, 0.88192126434835483f, 0.92387953251128652f, 0.95694033573220882f, 0.98078528040323032f, 0.99518472667219693f};
+  static constexpr float s[64] = {0.0f, 0.098017140329560604f, 0.19509032201612825f, 0.29028467725446233f, 0.38268343236508978f, 0.47139673682599764f, 0.55557023301960218f, 0.63439328416364549f, 0.70710678118654746f, 0.77301045336273699f, 0.83146961230254524f, 0.88192126434835494f, 0.92387953251128674f, 0.95694033573220894f, 0.98078528040323043f, 0.99518472667219682f, 1.0f, 0.99518472667219693f, 0.98078528040323043f, 0.95694033573220894f, 0.92387953251128674f, 0.88192126434835505f, 0.83146961230254546f, 0.7730104533627371f, 0.70710678118654757f, 0.63439328416364549f, 0.55557023301960218f, 0.47139673682599786f, 0.38268343236508989f, 0.29028467725446239f, 0.19509032201612861f, 0.098017140329560826f, 0.0f, -0.09801714032956059f, -0.19509032201612836f, -0.29028467725446211f, -0.38268343236508967f, -0.47139673682599764f, -0.55557023301960196f, -0.63439328416364527f, -0.70710678118654746f, -0.77301045336273666f, -0.83146961230254524f, -0.88192126434835494f, -0.92387953251128652f, -0.95694033573220882f, -0.98078528040323032f, -0.99518472667219693f, -1.0f, -0.99518472667219693f, -0.98078528040323043f, -0.95694033573220894f, -0.92387953251128663f, -0.88192126434835505f, -0.83146961230254546f, -0.77301045336273688f, -0.70710678118654768f, -0.63439328416364593f, -0.55557023301960218f, -0.47139673682599792f, -0.38268343236509039f, -0.2902846772544625f, -0.19509032201612872f, -0.098017140329560506f};
+};
+
+// v * W_R^E with compile-time R | 64 and E (forward sign unless INV)
 template <int R, int E, bool INV>
 __device__ __forceinline__ float2 twc(float2 v) {
   constexpr int e = ((E % R) + R) % R;
@@ -62,18 +68,18 @@ __device__ __forceinline__ float2 twc(float2 v) {
     return mul_q1<!INV>(v);
   } else if constexpr (8 * e == R || 8 * e == 3 * R || 8 * e == 5 * R || 8 * e == 7 * R) {
     // odd multiples of pi/4: (+-1 +- i)/sqrt2 -> 2 adds + 2 muls
-    constexpr int k = e * (16 / R);
-    constexpr float c = Trig16::c[k];
-    constexpr float s = INV ? Trig16::s[k] : -Trig16::s[k];
+    constexpr int k = e * (64 / R);
+    constexpr float c = Trig64::c[k];
+    constexpr float s = INV ? Trig64::s[k] : -Trig64::s[k];
     // (x + iy)(c + is) with |c| = |s| = 1/sqrt2
     constexpr float h = 0.70710678118654752f;
     constexpr float sc = c > 0 ? 1.0f : -1.0f;
     constexpr float ss = s > 0 ? 1.0f : -1.0f;
     return make_float2((sc * v.x - ss * v.y) * h, (ss * v.x + sc * v.y) * h);
   } else {
-    constexpr int k = e * (16 / R);
-    constexpr float c = Trig16::c[k];
-    constexpr float s = INV ? Trig16::s[k] : -Trig16::s[k];
+    constexpr int k = e * (64 / R);
+    constexpr float c = Trig64::c[k];
+    constexpr float s = INV ? Trig64::s[k] : -Trig64::s[k];
     return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
   }
 }
@@ -186,6 +192,10 @@ struct DftHalf {
 };
 
 __device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
+// padding of the exchange buffer: one element per PB (16, or the radix when
+// it is larger), conflict-free for the strided Stockham stores
+template <int PB>
+__device__ __forceinline__ int spadb(int i) { return i + i / PB; }
 // spad(i + c) for a compile-time c that is a multiple of 16: spad(i) + 17 c / 16
 // (lets every buffer access share one per-thread base + an immediate offset)
 template <int C>
@@ -239,7 +249,8 @@ __host__ __device__ constexpr int default_rpt(int n) { return n < 16 ? n : 16; }
 template <int N, int RPT_ = default_rpt(N)>
 struct FftShape {
   static_assert((N & (N - 1)) == 0 && N >= 2, "power of two");
-  static_assert((RPT_ & (RPT_ - 1)) == 0 && RPT_ >= 2 && RPT_ <= 16 && RPT_ <= N, "points per thread");
+  static_assert((RPT_ & (RPT_ - 1)) == 0 && RPT_ >= 2 && (RPT_ <= 16 || RPT_ == 64) && RPT_ <= N,
+                "points per thread");
   static constexpr int RPT = RPT_;             // points per thread
   static constexpr int TPF = N / RPT;          // threads per transform
   static constexpr int P = ilog2(N);
@@ -247,7 +258,8 @@ struct FftShape {
   static constexpr int NFULL = P / LR;                              // radix-RPT passes
   static constexpr int REM = 1 << (P % LR);                         // remainder radix (last)
   static constexpr int NPASS = NFULL + (REM > 1 ? 1 : 0);
-  static constexpr int SMEM = NPASS > 1 ? N + N / 16 : 0;          // float2 elements
+  static constexpr int PB = RPT > 16 ? RPT : 16;                    // exchange-buffer pad block
+  static constexpr int SMEM = NPASS > 1 ? N + N / PB : 0;          // float2 elements
   __host__ __device__ static constexpr int radix(int p) { return p < NFULL ? RPT : REM; }
   __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : ns(p - 1) * radix(p - 1); }
 };
@@ -288,8 +300,9 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
   float2 x[PER][R];
   // loads t + b TPF + m NB: one padded base per thread when TPF and NB are
   // multiples of 16 (N >= 256), else the padding per element
-  constexpr bool ALIGNED = (S::TPF % 16 == 0) && (NB % 16 == 0);
-  const int sp_t = spad(t);
+  constexpr int PB = S::PB;
+  constexpr bool ALIGNED = (S::TPF % PB == 0) && (NB % PB == 0);
+  const int sp_t = spadb<PB>(t);
 #pragma unroll
   for (int b = 0; b < PER; ++b)
 #pragma unroll
@@ -297,9 +310,9 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
       if constexpr (FIRST) {
         x[b][m] = v[b + m * PER];
       } else if constexpr (ALIGNED) {
-        x[b][m] = active ? buf[sp_t + (b * S::TPF + m * NB) + (b * S::TPF + m * NB) / 16] : make_float2(0.f, 0.f);
+        x[b][m] = active ? buf[sp_t + (b * S::TPF + m * NB) + (b * S::TPF + m * NB) / PB] : make_float2(0.f, 0.f);
       } else {
-        x[b][m] = active ? buf[spad(t + b * S::TPF + m * NB)] : make_float2(0.f, 0.f);
+        x[b][m] = active ? buf[spadb<PB>(t + b * S::TPF + m * NB)] : make_float2(0.f, 0.f);
       }
     }
   if constexpr (!FIRST) sync();
@@ -321,7 +334,19 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
       x[b][1] = cmul(x[b][1], w);
       if constexpr (R > 2) x[b][2] = cmul(x[b][2], w2);
       if constexpr (R > 3) x[b][3] = cmul(x[b][3], w3);
-      if constexpr (R > 4) {
+      if constexpr (R > 16) {
+        // 64-point passes: w^(4a) by a running product
+        const float2 w4 = cmul(w2, w2);
+        float2 w4k = w4;
+#pragma unroll
+        for (int k = 4; k < R; k += 4) {
+          if (k > 4) w4k = cmul(w4k, w4);
+          x[b][k] = cmul(x[b][k], w4k);
+          x[b][k + 1] = cmul(x[b][k + 1], cmul(w4k, w));
+          x[b][k + 2] = cmul(x[b][k + 2], cmul(w4k, w2));
+          x[b][k + 3] = cmul(x[b][k + 3], cmul(w4k, w3));
+        }
+      } else if constexpr (R > 4) {
         float2 w4k = cmul(w2, w2);
 #pragma unroll
         for (int k = 4; k < R; k += 4) {
@@ -345,15 +370,15 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[FftShape<N, RP>::RPT], floa
       for (int m = 0; m < R; ++m) v[b + m * PER] = x[b][m];
     } else if (active) {
       const int base = (j / NS) * NS * R + k;
-      if constexpr (NS % 16 == 0 || (NS == 1 && R == 16)) {
-        // base + m NS never carries into the padding index beyond m NS / 16
-        // (NS % 16 == 0), or base is a multiple of 16 and m < 16 (NS == 1)
-        const int sp_b = spad(base);
+      if constexpr (NS % PB == 0 || (NS == 1 && R == PB)) {
+        // base + m NS never carries into the padding index beyond m NS / PB
+        // (NS % PB == 0), or base is a multiple of PB and m < PB (NS == 1)
+        const int sp_b = spadb<PB>(base);
 #pragma unroll
-        for (int m = 0; m < R; ++m) buf[sp_b + m * NS + (m * NS) / 16] = x[b][m];
+        for (int m = 0; m < R; ++m) buf[sp_b + m * NS + (m * NS) / PB] = x[b][m];
       } else {
 #pragma unroll
-        for (int m = 0; m < R; ++m) buf[spad(base + m * NS)] = x[b][m];
+        for (int m = 0; m < R; ++m) buf[spadb<PB>(base + m * NS)] = x[b][m];
       }
     }
   }

@@ -113,6 +113,27 @@ struct KShape {
   static constexpr int MINB = THREADS <= 256 ? TB_MINB : 1;
 };
 
+// K1's transform shape: TB_K1_RPT = 64 puts 64 points in each thread's
+// registers (4096 = 64 x 64: one shared-memory exchange per transform instead
+// of two, 64 threads per row pair); default 16 as everywhere else
+#ifndef TB_K1_RPT
+#define TB_K1_RPT 16
+#endif
+template <int L>
+struct K1Shape {
+  static constexpr int RPT = (TB_K1_RPT == 64 && L >= 4096) ? 64 : default_rpt(L);
+  using S = FftShape<L, RPT>;
+  static constexpr int TPF = S::TPF;
+  static constexpr int THREADS = TPF < 32 ? 32 : TPF;
+  static constexpr int BUF = S::SMEM > 0 ? S::SMEM : L;
+  static constexpr int PB = S::PB;
+  static constexpr int LPB = ilog2(PB);
+#ifndef TB_K1_MINB64
+#define TB_K1_MINB64 4
+#endif
+  static constexpr int MINB = THREADS <= 64 ? TB_K1_MINB64 : (THREADS <= 256 ? 4 : 1);
+};
+
 // ---------------------------------------------------------------------------
 // Normalisation prologue (preprocess.py:59-74): transmission counts to line
 // integrals, y = -ln(max(I - D, eps) / max(I0 - D, eps)).  nt = (D, 1 /
@@ -137,8 +158,8 @@ __device__ __forceinline__ float norm_line(float I, float2 nt, float eps) {
 template <int L, bool RAMP, bool NORM, bool PRE = false>
 __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restrict__ sino, const Work& w, int g, int q,
                                          float2* smem) {
-  using K = KShape<L>;
-  constexpr int RPT = K::RPT, TPF = K::TPF;
+  using K = K1Shape<L>;
+  constexpr int RPT = K::RPT, TPF = K::TPF, PB = K::PB;
   float2* buf = smem;
   float* sacc = reinterpret_cast<float*>(smem + K::BUF);
   // staging for the row pair (TMA bulk copies, TB_K1_SLOTS > 0), 16-B
@@ -263,13 +284,13 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
       }
     }
     if constexpr (RAMP) {
-      fft_half<L, false>(v, buf, t, active, p.tw_np);
+      fft_half<L, false, CtaSync, RPT>(v, buf, t, active, p.tw_np);
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
         const float gk = active ? __ldg(p.ramp_g + t + i * TPF) : 0.f;
         v[i] = cscale(v[i], gk);
       }
-      fft<L, true>(v, buf, t, active, p.tw_np);
+      fft<L, true, CtaSync, RPT>(v, buf, t, active, p.tw_np);
     }
     // v[i] = (h_j0, h_j1)(t_idx) for idx < n_t: support sums, window, zero pad
 #pragma unroll
@@ -284,19 +305,19 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
         v[i] = cscale(v[i], m);
       }
     }
-    fft_half<L, false>(v, buf, t, active, p.tw_L);
+    fft_half<L, false, CtaSync, RPT>(v, buf, t, active, p.tw_L);
     // exchange Z_k / Z_{L-k} through smem to separate the two real rows
-    constexpr bool XALIGN = FftShape<L>::SMEM > 0 && (TPF % 16 == 0);
+    constexpr bool XALIGN = K::S::SMEM > 0 && (TPF % PB == 0);
     if constexpr (XALIGN) {
-      const int sp_t = spad(t);
+      const int sp_t = spadb<PB>(t);
       if (active) {
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) buf[sp_t + i * TPF + (i * TPF) / 16] = v[i];
+        for (int i = 0; i < RPT; ++i) buf[sp_t + i * TPF + (i * TPF) / PB] = v[i];
       }
-    } else if constexpr (FftShape<L>::SMEM > 0) {
+    } else if constexpr (K::S::SMEM > 0) {
       if (active) {
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) buf[spad(t + i * TPF)] = v[i];
+        for (int i = 0; i < RPT; ++i) buf[spadb<PB>(t + i * TPF)] = v[i];
       }
     } else {
       if (active) {
@@ -328,11 +349,11 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
           const float2 zk = v[i];
           float2 zm;
           if constexpr (XALIGN) {
-            // spad(L - t - i TPF) = spad(-t) + (L - i TPF) 17 / 16 for k > 0
+            // spadb(L - t - i TPF) = spadb(-t) + (L - i TPF) (PB + 1) / PB for k > 0
             const int c = L - i * TPF;
-            zm = k == 0 ? buf[0] : buf[(-t) + ((-t) >> 4) + c + c / 16];
+            zm = k == 0 ? buf[0] : buf[(-t) + ((-t) >> K::LPB) + c + c / PB];
           } else {
-            zm = buf[FftShape<L>::SMEM > 0 ? spad(km) : km];
+            zm = buf[K::S::SMEM > 0 ? spadb<PB>(km) : km];
           }
           const float2 X = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
           const float2 Y = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
@@ -361,7 +382,8 @@ __device__ __forceinline__ void k1_block(const DevPlan& p, const float* __restri
 // PRE: the fused centre / ring stages on the row load (its own
 // instantiation: the plain load keeps its schedule, 0.45 ms per 2048^3)
 template <int L, bool RAMP, bool NORM, bool PRE = false>
-__global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_K1_MINB : 1)
+__global__ void __launch_bounds__(K1Shape<L>::THREADS, K1Shape<L>::THREADS <= 64 ? TB_K1_MINB64
+                                                    : (K1Shape<L>::THREADS <= 256 ? TB_K1_MINB : 1))
     k1_radial(DevPlan p, const float* __restrict__ sino, Work w) {
   extern __shared__ float2 smem[];
   k1_block<L, RAMP, NORM, PRE>(p, sino, w, blockIdx.x, blockIdx.y, smem);
@@ -1410,7 +1432,7 @@ __device__ __forceinline__ bool bres_take(long long x, long long n, long long T,
 template <int L, bool CROP_HALF, bool NORM>
 __global__ void __launch_bounds__(KShape<L>::THREADS, KShape<L>::THREADS <= 256 ? TB_KF_MINB : 1)
     kf_fused(DevPlan p, FusedArgs a) {
-  static_assert(KShape<L>::THREADS == K2Shape<L>::THREADS, "fused CTAs share one block size");
+  static_assert(K1Shape<L>::THREADS == K2Shape<L>::THREADS, "fused CTAs share one block size");
   extern __shared__ float2 smem[];
   const long long x = blockIdx.x;
   long long i3, i1;

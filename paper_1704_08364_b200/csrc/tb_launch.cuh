@@ -65,7 +65,7 @@ struct Launch {
   using K = tb::KShape<L>;
   static size_t smem_k1(const tb_plan* p) {
     // FFT buffer + support sums + TB_K1_SLOTS TMA staging slots of a row pair + 2 mbarriers
-    return K::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 +
+    return tb::K1Shape<L>::BUF * sizeof(float2) + (size_t)((std::max(p->S, 1) + 3) & ~3) * 4 +
            (size_t)K1_STAGE_ROWS * p->n_t * 4 + 16;
   }
   static size_t smem_k1b(const tb_plan* p) {
@@ -151,7 +151,7 @@ struct Launch {
     TB_CUDA(cudaFuncSetAttribute(tb::k1b_common<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1b));
     TB_CUDA(set_k2_smem<false>());
     TB_CUDA(cudaFuncSetAttribute(tb::k3_rows<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fft()));
-    if constexpr (tb::KShape<L>::THREADS == tb::K2Shape<L>::THREADS && L >= 64) {
+    if constexpr (tb::KShape<L>::THREADS == tb::K2Shape<L>::THREADS && tb::K1Shape<L>::THREADS == tb::K2Shape<L>::THREADS && L >= 64) {
       const int sf = (int)std::max({smem_k1(&worst), smem_k2(), smem_fft()});
       const int sfm = std::min(sf, smax);
       TB_CUDA(cudaFuncSetAttribute(tb::kf_fused<L, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sfm));
@@ -211,13 +211,13 @@ struct Launch {
     dim3 g1(p->groups, B);
     mark(1, 0);
     if (fused && wk.norm_eps > 0.f)  // transmission counts: normalisation fused into the load
-      tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
+      tb::k1_radial<L, true, true><<<g1, tb::K1Shape<L>::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else if (fused && wk.pre_shift)  // centre / ring stages fused into the load (tb_fbp_pre)
-      tb::k1_radial<L, true, false, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
+      tb::k1_radial<L, true, false, true><<<g1, tb::K1Shape<L>::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else if (fused)
-      tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
+      tb::k1_radial<L, true, false><<<g1, tb::K1Shape<L>::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     else
-      tb::k1_radial<L, false, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
+      tb::k1_radial<L, false, false><<<g1, tb::K1Shape<L>::THREADS, smem_k1(p), st>>>(dp, k1_in, wk);
     mark(1, 1);
     mark(2, 0);
     tb::k1b_common<L><<<B, K::K1B_THREADS, smem_k1b(p), st>>>(dp, w);
@@ -262,7 +262,7 @@ struct Launch {
   static int fused_pipeline(const tb_plan* p, const float* sino, float* img, int n_slices, int batch,
                             const Work* lanes, size_t in_stride, size_t out_stride, float scale, bool with_k3,
                             cudaStream_t st) {
-    if constexpr (tb::KShape<L>::THREADS != tb::K2Shape<L>::THREADS || L < 64) {
+    if constexpr (tb::K1Shape<L>::THREADS != tb::K2Shape<L>::THREADS || tb::KShape<L>::THREADS != tb::K2Shape<L>::THREADS || L < 64) {
       return TB_ERR_UNSUPPORTED;
     } else {
       const DevPlan& dp = p->dp;
@@ -279,9 +279,9 @@ struct Launch {
       {
         const dim3 g1(p->groups, nb(0));
         if (norm)
-          tb::k1_radial<L, true, true><<<g1, K::THREADS, smem_k1(p), st>>>(dp, sino, lanes[0]);
+          tb::k1_radial<L, true, true><<<g1, tb::K1Shape<L>::THREADS, smem_k1(p), st>>>(dp, sino, lanes[0]);
         else
-          tb::k1_radial<L, true, false><<<g1, K::THREADS, smem_k1(p), st>>>(dp, sino, lanes[0]);
+          tb::k1_radial<L, true, false><<<g1, tb::K1Shape<L>::THREADS, smem_k1(p), st>>>(dp, sino, lanes[0]);
         tb::k1b_common<L><<<nb(0), K::K1B_THREADS, smem_k1b(p), st>>>(dp, lanes[0]);
       }
       const size_t smem = std::max({smem_k1(p), smem_k2(), smem_fft()});
