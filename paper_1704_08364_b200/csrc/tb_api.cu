@@ -902,17 +902,19 @@ int tb_forward(const tb_plan* p, const float* image, float* sino, int n_slices, 
   const int m = (int)std::ceil(2.0 * std::sqrt(2.0) / h);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t nn = (size_t)p->n * p->n;
-  // bilinear: TLD4 gathers from a pitch-2D texture over runs of slices
-  // (image_texture; rows <= the pitch-2D height limit); nearest, or an
-  // image the texture unit cannot view, takes the plain-load kernel
+  // TLD4 gathers (bilinear) or point fetches (nearest) from a pitch-2D
+  // texture over runs of slices (image_texture; rows <= the pitch-2D height
+  // limit); an image the texture unit cannot view takes the plain-load kernel
   const int per_tex = std::max(1, 65000 / p->n);
   for (int s = 0; s < n_slices;) {
     const int B = std::min(std::min(65535, per_tex), n_slices - s);
     const float* im = image + (size_t)s * nn;
     dim3 grid((p->n_t + 127) / 128, p->rows, B);
-    cudaTextureObject_t tex = interp == TB_INTERP_BILINEAR ? image_texture(p, im, B * p->n) : 0;
-    if (tex)
-      tb::k6_forward_tex<<<grid, 128, 0, st>>>(p->dp, tex, sino + (size_t)s * p->rows * p->n_t, p->rows, h, m);
+    cudaTextureObject_t tex = image_texture(p, im, B * p->n);
+    if (tex && interp == TB_INTERP_NEAREST)
+      tb::k6_forward_tex<true><<<grid, 128, 0, st>>>(p->dp, tex, sino + (size_t)s * p->rows * p->n_t, p->rows, h, m);
+    else if (tex)
+      tb::k6_forward_tex<false><<<grid, 128, 0, st>>>(p->dp, tex, sino + (size_t)s * p->rows * p->n_t, p->rows, h, m);
     else
       tb::k6_forward<<<grid, 128, 0, st>>>(p->dp, im, sino + (size_t)s * p->rows * p->n_t, p->rows, h, m,
                                             interp == TB_INTERP_NEAREST ? 1 : 0);

@@ -1744,6 +1744,9 @@ __global__ void __launch_bounds__(128) k6_forward(DevPlan p, const float* __rest
 // are rounded to fp32 (<= 6e-8) and the sum runs in fp64.  Rows outside the
 // slice (y0 = -1 or y0 + 1 = n lie in the neighbouring slice of the
 // texture) are masked explicitly.
+// NEAREST: one point fetch per sample at np.rint of the fp64 position (4 B
+// of texture return instead of the 16 B footprint)
+template <bool NEAREST>
 __global__ void __launch_bounds__(128) k6_forward_tex(DevPlan p, cudaTextureObject_t tex, float* __restrict__ sino,
                                                       int n_ang, double h, int m) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1778,6 +1781,14 @@ __global__ void __launch_bounds__(128) k6_forward_tex(DevPlan p, cudaTextureObje
       const double ell = -half + ((double)k + 0.5) * h;
       const double fx = (t * cs.x - ell * cs.y + 1.0) * inv_du - 0.5;
       const double fy = (t * cs.y + ell * cs.x + 1.0) * inv_du - 0.5;
+      if constexpr (NEAREST) {
+        const double ixf = rint(fx), iyf = rint(fy);
+        const int iy = (int)iyf;
+        // columns outside read the border (0); rows outside the slice are masked
+        const float v = tex2D<float>(tex, (float)(ixf + 0.5), ybase - 0.5f + (float)iy);
+        if (iy >= 0 && iy < n) acc += (double)v;
+        continue;
+      }
       const double x0f = floor(fx), y0f = floor(fy);
       const int y0 = (int)y0f;
       const float wx = (float)(fx - x0f), wy = (float)(fy - y0f);

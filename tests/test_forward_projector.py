@@ -114,7 +114,8 @@ def test_gpu_forward_batched_linearity_1024():
 
 
 @pytest.mark.gpu
-def test_gpu_forward_texture_path_chunks_and_plain_fallback(monkeypatch):
+@pytest.mark.parametrize("nearest", [False, True])
+def test_gpu_forward_texture_path_chunks_and_plain_fallback(monkeypatch, nearest):
     """The bilinear forward projector reads images through pitch-2D texture
     views of up to 65000 rows (31 slices at n = 2048): a 33-slice call spans
     two views, and slices 30 / 31 / 32 sit on the view boundaries, whose
@@ -129,13 +130,13 @@ def test_gpu_forward_texture_path_chunks_and_plain_fallback(monkeypatch):
     g = torch.Generator("cuda").manual_seed(3)
     imgs = torch.rand((S, n, n), device="cuda", generator=g)
     out = torch.empty((S, v, n_t), device="cuda")
-    nat.forward(imgs, out, S)
+    nat.forward(imgs, out, S, 0.5, nearest)
     for k in (0, 29, 30, 31, 32):
         one = torch.empty((1, v, n_t), device="cuda")
-        nat.forward(imgs[k:k + 1].contiguous(), one, 1)
+        nat.forward(imgs[k:k + 1].contiguous(), one, 1, 0.5, nearest)
         assert torch.equal(one[0], out[k]), k
     monkeypatch.setenv("TB_NOTEX", "1")
     plain = torch.empty((2, v, n_t), device="cuda")
-    nat.forward(imgs[30:32].contiguous(), plain, 2)
+    nat.forward(imgs[30:32].contiguous(), plain, 2, 0.5, nearest)
     d = torch.linalg.norm(plain - out[30:32]) / torch.linalg.norm(out[30:32])
     assert d.item() < 1e-6
