@@ -263,3 +263,19 @@ def test_fbp_stage_with_center_and_rings_against_oracle(center):
         beta = O.estimate_center(host[i])[0] if center == "auto" else center
         pre = O.suppress_rings(O.apply_center(host[i], beta), 9)
         _assert_close(img.data, O.fbp(pre, op))
+
+
+@pytest.mark.parametrize("full,interp", [(True, "bilinear"), (False, "nearest")])
+def test_texture_paths_at_2048_against_oracle(full, interp):
+    """K2_TEXF / K2_TEXN at the headline size (L = 4096, the 5-CTA kernels,
+    thread-0 mirror bookkeeping at 256 threads per column): the last slice
+    of a 17-slice volume (two launch groups for full turn) vs the oracle."""
+    F = _F()
+    N, S = 2048, 17
+    plan = F.BstPlan(N, N, interp=interp)
+    A = 2 * N if full else N
+    g = torch.Generator("cuda").manual_seed(17)
+    vol = torch.randn((S, A, N), device="cuda", generator=g)
+    out = F.fbp_volume(vol, plan, full_turn=full)
+    ref = O.fbp(vol[S - 1].cpu().numpy().astype(np.float64), O.OraclePlan(N, N, interp=interp), full_turn=full)
+    _assert_close(out[S - 1].cpu().numpy(), ref)
